@@ -1,0 +1,178 @@
+"""Generate the golden fixtures under tests/golden/ by importing the REFERENCE.
+
+Run in the build container (the reference is mounted read-only at
+/root/reference; it does not exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Every number in the fixtures comes from the reference package ``neoxfuse``
+itself (``/root/reference/pkg/src/neoxfuse``).  The fixtures pin the CPU
+oracle (``oracle/neox_oracle.py``) -- see ``tests/test_oracle_golden.py`` --
+and, through the oracle, the GPU parity tests.
+"""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.dont_write_bytecode = True
+REF = os.environ.get("NEOXFUSE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+import numpy as np  # noqa: E402
+
+import neoxfuse as nf  # noqa: E402
+from neoxfuse import halfnum  # noqa: E402
+from neoxfuse.cluster import ClusterSpec, fused_block_step  # noqa: E402
+from neoxfuse.config import ModelConfig, preset  # noqa: E402
+from neoxfuse.golden import decoder_block_golden  # noqa: E402
+from neoxfuse.plans import plan_baseline, plan_full_fused, kernel_layer_bytes  # noqa: E402
+from neoxfuse.weights import KVCache, synth_weights, TENSOR_NAMES  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+C1 = dict(hidden=768, n_heads=12, d_head=64, n_layers=12, d_mlp=3072,
+          rotary_pct=0.25, vocab=50304)
+D80 = dict(hidden=1280, n_heads=16, d_head=80, n_layers=1, d_mlp=5120,
+           rotary_pct=0.25, vocab=512)
+SEQ = dict(hidden=512, n_heads=8, d_head=64, n_layers=1, d_mlp=2048,
+           rotary_pct=0.25, vocab=256, parallel_residual=False)
+
+
+def f16(w):
+    """Round every tensor of a BlockWeights through binary16 (reference RNE)."""
+    return nf.BlockWeights(**{n: halfnum.half_round_array(getattr(w, n))
+                              for n in TENSOR_NAMES})
+
+
+def prng():
+    seeds = np.array([0, 1, 12345, (1 << 63) + 5, (1 << 64) - 1], dtype=np.uint64)
+    counters = np.concatenate([
+        np.arange(64, dtype=np.uint64),
+        (np.uint64(7) << np.uint64(32)) + np.arange(64, dtype=np.uint64),
+        np.array([(1 << 40) + 3, (11 << 32) + 123456789], dtype=np.uint64),
+    ])
+    draws = np.stack([halfnum.counter_rand_u64_array(int(s), counters) for s in seeds])
+    scalar = np.array([halfnum.counter_rand_u64(int(seeds[2]), int(c)) for c in counters[:8]],
+                      dtype=np.uint64)
+    np.savez(OUT / "prng.npz", seeds=seeds, counters=counters, draws=draws, scalar=scalar)
+
+
+def half():
+    rng = np.random.default_rng(0)
+    x = np.concatenate([
+        rng.standard_normal(4000) * 10.0 ** rng.integers(-9, 6, 4000),
+        # exact binary16 ties and neighbours, subnormal range, overflow edge
+        (np.arange(-2048, 2048) + 0.5) * 2.0 ** -10,
+        (np.arange(0, 512) + 0.5) * 2.0 ** -24,
+        np.array([65504.0, 65519.99, 65520.0, 1e6, -1e6, 0.0, -0.0, 2.0 ** -25,
+                  2.0 ** -25 * 1.0000001, 2.0 ** -26, 6.1e-5, 5.96e-8]),
+    ])
+    np.savez(OUT / "half.npz", x=x, y=halfnum.half_round_array(x),
+             bits=np.array([halfnum.half_round(v).bits for v in x[:64]]))
+
+
+def synth():
+    out = {}
+    rng = np.random.default_rng(1)
+    for tag, cfg, seed in (("tiny", preset("tiny"), 5), ("c1", ModelConfig(**C1), 0),
+                           ("d80", ModelConfig(**D80), 3)):
+        w = synth_weights(cfg, seed)
+        for n in TENSOR_NAMES:
+            a = getattr(w, n).ravel()
+            idx = rng.integers(0, a.size, 64)
+            out[f"{tag}.{n}.sum"] = np.array(np.sum(a))
+            out[f"{tag}.{n}.idx"] = idx
+            out[f"{tag}.{n}.val"] = a[idx]
+            out[f"{tag}.{n}.head"] = a[:16]
+            out[f"{tag}.{n}.tail"] = a[-16:]
+            out[f"{tag}.{n}.f16sum"] = np.array(np.sum(halfnum.half_round_array(a)))
+    np.savez(OUT / "synth.npz", **out)
+
+
+def _prefix(rng, cfg, n):
+    pk = rng.standard_normal((cfg.n_heads, n, cfg.d_head)) * 0.5
+    pv = rng.standard_normal((cfg.n_heads, n, cfg.d_head)) * 0.5
+    return halfnum.half_round_array(pk), halfnum.half_round_array(pv)
+
+
+def blocks():
+    """decoder_block_golden / fused_block_step runs on fp16-rounded weights.
+
+    Input recipe (re-created by the tests): rng = default_rng(seed);
+    prefix K, V = N(0,1)*0.5 [H, prefix, d] rounded to fp16; then per step
+    x_t = N(0,1)*0.5 [hidden]."""
+    cases = {
+        "c1": (ModelConfig(**C1), 0, 128, 1, "tanh"),
+        "c1exact": (ModelConfig(**C1), 0, 128, 1, "exact"),
+        "d80": (ModelConfig(**D80), 3, 40, 3, "tanh"),
+        "seq": (ModelConfig(**SEQ), 4, 17, 2, "exact"),
+        "p0": (ModelConfig(**C1), 6, 0, 3, "tanh"),
+        "wide": (preset("pythia-2.8b").with_(n_layers=1), 9, 3, 1, "tanh"),
+    }
+    for tag, (cfg, seed, npre, steps, gelu) in cases.items():
+        w = f16(synth_weights(cfg, seed))
+        rng = np.random.default_rng(seed)
+        pk, pv = _prefix(rng, cfg, npre)
+        xs = rng.standard_normal((steps, cfg.hidden)) * 0.5
+        cache = KVCache.from_arrays(pk, pv) if npre else KVCache(cfg.n_heads, cfg.d_head)
+        fcache = KVCache.from_arrays(pk, pv) if npre else KVCache(cfg.n_heads, cfg.d_head)
+        outs, fouts = [], []
+        for t in range(steps):
+            outs.append(decoder_block_golden(xs[t], w, cache, npre + t, cfg, gelu))
+            o, tr = fused_block_step(xs[t], w, fcache, npre + t, cfg, ClusterSpec(n_blocks=4),
+                                     plan_full_fused(), gelu)
+            fouts.append(o)
+        keys, vals = cache.keys(), cache.values()
+        np.savez(OUT / f"block_{tag}.npz", seed=seed, prefix=npre, steps=steps,
+                 gelu=gelu, model=json.dumps({k: getattr(cfg, k) for k in (
+                     "hidden", "n_heads", "d_head", "n_layers", "d_mlp", "rotary_pct",
+                     "vocab", "ln_eps", "theta_base", "parallel_residual")}),
+                 xs=xs, outs=np.array(outs), fused=np.array(fouts),
+                 new_keys=keys[:, npre:], new_values=vals[:, npre:],
+                 trace_offchip=tr.bytes_offchip, trace_onchip=tr.bytes_onchip,
+                 trace_sync=tr.sync_steps, trace_dsmem=tr.dsmem_exchanges)
+
+
+def fidelity():
+    out = {}
+    for seed in range(3):
+        inst = nf.synthetic_instance(seed)
+        out[f"syn{seed}.golden"] = inst.golden_logits()
+        out[f"syn{seed}.exact"] = inst.variant_logits(ClusterSpec(n_blocks=4))
+    adv = nf.adversarial_instance()
+    out["adv.golden"] = adv.golden_logits()
+    # a 160M-shape probe instance: 1 block, prompt 16, 6 teacher-forced steps
+    cfg = ModelConfig(**C1).with_(n_layers=1, vocab=1000)
+    inst = nf.synthetic_instance(21, cfg, prompt_len=16, steps=6)
+    out["c1probe.golden"] = inst.golden_logits()
+    rep = nf.compare(out["syn0.golden"], out["syn0.golden"] + np.linspace(0, 1e-3, 11))
+    out["compare.syn0"] = np.array([rep.token_match_rate, rep.logits_mae,
+                                    rep.topk_agreement[5], rep.topk_agreement[10]])
+    np.savez(OUT / "fidelity.npz", **out)
+
+
+def bytes_model():
+    doc = {}
+    for name, cfg in (("pythia-2.8b", preset("pythia-2.8b")), ("pythia-6.9b", preset("pythia-6.9b")),
+                      ("c1", ModelConfig(**C1).with_(n_layers=1))):
+        for P in (1, 129, 1025, 1152, 2049, 4097):
+            tr = nf.traffic(plan_full_fused(), cfg, P)
+            doc[f"{name}.full.{P}"] = [tr.layer_bytes, tr.lm_head_bytes, tr.step_bytes]
+            doc[f"{name}.baseline.{P}"] = kernel_layer_bytes(plan_baseline(), cfg, P)
+        pc = nf.count_params(cfg)
+        doc[f"{name}.params"] = [pc.per_layer, pc.blocks, pc.final_ln, pc.unembedding]
+        doc[f"{name}.flops.1024"] = nf.flops_per_token(cfg, 1024)
+    doc["mlp_saving.2.8b"] = nf.mlp_fusion_saving_bytes(preset("pythia-2.8b"))
+    (OUT / "bytes.json").write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")
+
+
+if __name__ == "__main__":
+    prng()
+    half()
+    synth()
+    blocks()
+    fidelity()
+    bytes_model()
+    print("golden fixtures written to", OUT)

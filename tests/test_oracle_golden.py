@@ -1,0 +1,163 @@
+"""Pin the CPU oracle against golden vectors generated from the reference.
+
+The fixtures were produced by importing the reference package itself
+(tests/golden/make_golden.py); nothing here reads /root/reference.
+"""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import neox_oracle as O
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(G, name), allow_pickle=False)
+
+
+def shape_of(fx):
+    return O.Shape(**json.loads(str(fx["model"])))
+
+
+def test_splitmix64_bit_exact():
+    f = load("prng.npz")
+    for s, row in zip(f["seeds"], f["draws"]):
+        assert np.array_equal(O.splitmix64(int(s), f["counters"]), row)
+    assert np.array_equal(O.splitmix64(int(f["seeds"][2]), f["counters"][:8]), f["scalar"])
+
+
+def test_half_rounding_bit_exact():
+    f = load("half.npz")
+    got = O.f16_round(f["x"])
+    want = f["y"]
+    both_nan = np.isnan(got) & np.isnan(want)
+    assert np.array_equal(got[~both_nan], want[~both_nan])
+    bits = f["x"][:64].astype(np.float16).view(np.uint16)
+    assert np.array_equal(bits, f["bits"].astype(np.uint16))
+
+
+@pytest.mark.parametrize("tag,cfg,seed", [
+    ("tiny", dict(hidden=8, n_heads=2, d_head=4, n_layers=2, d_mlp=16, rotary_pct=0.5, vocab=11), 5),
+    ("c1", dict(hidden=768, n_heads=12, d_head=64, n_layers=12, d_mlp=3072, rotary_pct=0.25, vocab=50304), 0),
+    ("d80", dict(hidden=1280, n_heads=16, d_head=80, n_layers=1, d_mlp=5120, rotary_pct=0.25, vocab=512), 3),
+])
+def test_synth_weights_bit_exact(tag, cfg, seed):
+    f = load("synth.npz")
+    p = O.synth_block(O.Shape(**cfg), seed)
+    for n in O.BLOCK_TENSORS:
+        a = p[n].ravel()
+        assert np.array_equal(a[f[f"{tag}.{n}.idx"]], f[f"{tag}.{n}.val"]), n
+        assert np.array_equal(a[:16], f[f"{tag}.{n}.head"]), n
+        assert np.array_equal(a[-16:], f[f"{tag}.{n}.tail"]), n
+        assert np.sum(a) == f[f"{tag}.{n}.sum"], n
+        assert np.sum(O.f16_round(a)) == f[f"{tag}.{n}.f16sum"], n
+
+
+def _replay(tag, ln=O.ln_two_pass):
+    fx = load(f"block_{tag}.npz")
+    s = shape_of(fx)
+    seed, npre, steps = int(fx["seed"]), int(fx["prefix"]), int(fx["steps"])
+    p = O.f16_params(O.synth_block(s, seed))
+    rng = np.random.default_rng(seed)
+    pk = O.f16_round(rng.standard_normal((s.n_heads, npre, s.d_head)) * 0.5)
+    pv = O.f16_round(rng.standard_normal((s.n_heads, npre, s.d_head)) * 0.5)
+    xs = rng.standard_normal((steps, s.hidden)) * 0.5
+    assert np.array_equal(xs, fx["xs"])
+    cache = O.KV.of(pk, pv) if npre else O.KV(s.n_heads, s.d_head)
+    outs = [O.block_step(xs[t], p, cache, npre + t, s, str(fx["gelu"]), ln) for t in range(steps)]
+    return fx, np.array(outs), cache
+
+
+@pytest.mark.parametrize("tag", ["c1", "c1exact", "d80", "seq", "p0"])
+def test_block_matches_reference_golden(tag):
+    fx, outs, cache = _replay(tag)
+    scale = np.max(np.abs(fx["outs"]))
+    assert np.max(np.abs(outs - fx["outs"])) <= 1e-12 * scale
+    npre = int(fx["prefix"])
+    assert np.max(np.abs(cache.keys()[:, npre:] - fx["new_keys"])) <= 1e-12
+    assert np.array_equal(cache.values()[:, npre:], fx["new_values"])
+
+
+@pytest.mark.parametrize("tag", ["c1", "d80", "seq"])
+def test_fused_semantics_match_reference(tag):
+    """Single-pass LN numerics of fused_block_step (EXACT) -- nf/cluster.py:316."""
+    fx, outs, _ = _replay(tag, O.ln_single_pass)
+    scale = np.max(np.abs(fx["fused"]))
+    assert np.max(np.abs(outs - fx["fused"])) <= 1e-11 * scale
+
+
+@pytest.mark.slow
+def test_wide_block_matches_reference_golden():
+    fx, outs, _ = _replay("wide")
+    assert np.max(np.abs(outs - fx["outs"])) <= 1e-12 * np.max(np.abs(fx["outs"]))
+
+
+def test_split_attention_equals_naive():
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 37, 130):
+        for blocks in (1, 2, 3, 4, 7):
+            q = rng.standard_normal(80)
+            k = rng.standard_normal((n, 80))
+            v = rng.standard_normal((n, 80))
+            a = O.attend(q, k, v, 1 / math.sqrt(80))
+            b = O.split_attend(q, k, v, blocks, 1 / math.sqrt(80))
+            assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(a)))
+
+
+def _instance(seed, s, prompt_len=12, steps=8):
+    """synthetic_instance recipe (nf/fidelity.py:156-170)."""
+    p = O.synth_block(s, seed)
+    rng = np.random.default_rng(seed)
+    unembed = rng.standard_normal((s.vocab, s.hidden))
+    xs = rng.standard_normal((steps, s.hidden)) * 0.5
+    pk = rng.standard_normal((s.n_heads, prompt_len, s.d_head)) * 0.5
+    pv = rng.standard_normal((s.n_heads, prompt_len, s.d_head)) * 0.5
+    return p, unembed, xs, pk, pv
+
+
+def _probe_logits(s, p, unembed, xs, pk, pv):
+    cache = O.KV.of(pk, pv)
+    out = []
+    for t, x in enumerate(xs):
+        out.append(unembed @ O.block_step(x, p, cache, pk.shape[1] + t, s))
+    return np.array(out)
+
+
+def test_decode_instance_golden_logits():
+    f = load("fidelity.npz")
+    tiny = O.Shape(8, 2, 4, 2, 16, 0.5, 11)
+    for seed in range(3):
+        got = _probe_logits(tiny, *_instance(seed, tiny))
+        assert np.max(np.abs(got - f[f"syn{seed}.golden"])) <= 1e-12 * np.max(np.abs(got))
+    c1 = O.Shape(768, 12, 64, 1, 3072, 0.25, 1000)
+    got = _probe_logits(c1, *_instance(21, c1, 16, 6))
+    assert np.max(np.abs(got - f["c1probe.golden"])) <= 1e-11 * np.max(np.abs(got))
+
+
+def test_ln_single_vs_two_pass_close():
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        x = rng.standard_normal(2560) * 3
+        g = 1 + 0.1 * rng.standard_normal(2560)
+        b = 0.1 * rng.standard_normal(2560)
+        a = O.ln_two_pass(x, g, b, 1e-5)
+        c = O.ln_single_pass(x, g, b, 1e-5)
+        assert np.max(np.abs(a - c)) <= 1e-9
+
+
+def test_oracle_errors_match_reference_messages():
+    s = O.Shape(768, 12, 64, 1, 3072, 0.25, 100)
+    p = O.synth_block(s, 0)
+    with pytest.raises(ValueError, match="cache holds 0 positions, expected 2"):
+        O.block_step(np.zeros(768), p, O.KV(12, 64), 2, s)
+    with pytest.raises(ValueError, match="input must have shape"):
+        O.block_step(np.zeros(5), p, O.KV(12, 64), 0, s)
+    x = np.zeros(768)
+    x[3] = np.nan
+    with pytest.raises(ValueError, match="non-finite activation"):
+        O.block_step(x, p, O.KV(12, 64), 0, s)
