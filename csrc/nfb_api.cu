@@ -1,0 +1,932 @@
+// C-ABI implementation (include/nfb200.h): context, parameter upload and
+// device-side synthesis, KV cache I/O, launch paths (eager, decode, graph).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../include/nfb200.h"
+#include "nfb_internal.h"
+
+namespace nfb {
+const void* decode_kernel_ptr(int dpl);
+cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
+                          bool cooperative);
+cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out);
+}  // namespace nfb
+
+using namespace nfb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(NFB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// binary16 round-to-nearest-even from float64 bits (IEEE 754; same results as
+// the reference's integer algorithm, nf/halfnum.py:80-111).
+__host__ __device__ inline uint16_t f64_to_f16_bits(double x) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  const uint16_t sign = (uint16_t)((b >> 48) & 0x8000u);
+  const int ex = (int)((b >> 52) & 0x7ff);
+  const uint64_t frac = b & 0xfffffffffffffull;
+  if (ex == 0x7ff) return frac ? 0x7e00 : (uint16_t)(sign | 0x7c00);
+  const int e = ex - 1023;
+  if (e >= 16) return (uint16_t)(sign | 0x7c00);
+  if (e >= -14) {
+    uint32_t hv = ((uint32_t)(e + 15) << 10) | (uint32_t)(frac >> 42);
+    const uint64_t rest = frac & ((1ull << 42) - 1);
+    const uint64_t tie = 1ull << 41;
+    if (rest > tie || (rest == tie && (hv & 1u))) ++hv;
+    return (uint16_t)(sign | hv);
+  }
+  if (e < -26) return sign;
+  const uint64_t sig = (1ull << 52) | frac;
+  const int sh = 28 - e;
+  uint64_t q = sig >> sh;
+  const uint64_t rest = sig & ((1ull << sh) - 1);
+  const uint64_t tie = 1ull << (sh - 1);
+  if (rest > tie || (rest == tie && (q & 1ull))) ++q;
+  return (uint16_t)(sign | q);
+}
+
+__host__ __device__ inline float f16_bits_to_f32(uint16_t hb) {
+  const uint32_t sign = (uint32_t)(hb & 0x8000u) << 16;
+  const uint32_t ex = (hb >> 10) & 0x1f, fr = hb & 0x3ffu;
+  float v;
+  if (ex == 0) {
+    v = (float)fr * 5.9604644775390625e-08f;  // 2^-24
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    u |= sign;
+    memcpy(&v, &u, 4);
+    return v;
+  }
+  uint32_t u = ex == 31 ? (sign | 0x7f800000u | (fr << 13)) : (sign | ((ex + 112) << 23) | (fr << 13));
+  memcpy(&v, &u, 4);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Counter PRNG: SplitMix64 output of seed + (counter+1)*gamma (nf/halfnum.py:35-45)
+__device__ __forceinline__ uint64_t splitmix(uint64_t seed, uint64_t c) {
+  uint64_t z = seed + (c + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// (u >> 11) * 2^-52 - 1, exact in f64 (nf/weights.py:58-62)
+__device__ __forceinline__ double uniform(uint64_t seed, uint32_t stream, uint64_t i) {
+  const uint64_t u = splitmix(seed, ((uint64_t)stream << 32) + i);
+  return __dadd_rn(__dmul_rn((double)(u >> 11), 0x1p-52), -1.0);
+}
+
+enum SynthKind : int { K_WEIGHT = 0, K_GAIN = 1, K_LNBIAS = 2, K_BIAS = 3, K_PLAIN = 4, K_KV = 5 };
+
+__device__ __forceinline__ double synth_value(int kind, double u, double div) {
+  switch (kind) {
+    case K_WEIGHT: return __ddiv_rn(u, div);                       // u / sqrt(fan_in)
+    case K_GAIN: return __dadd_rn(1.0, __dmul_rn(0.1, u));         // 1 + 0.1 u
+    case K_LNBIAS: return __dmul_rn(0.1, u);                       // 0.1 u
+    case K_BIAS: return __dmul_rn(0.02, u);                        // 0.02 u
+    case K_KV: return __dmul_rn(0.8660254037844386, u);            // var 0.25
+    default: return u;
+  }
+}
+
+// out[i] (or out[transposed i]) = fp16(synth(kind, uniform(seed, stream, i)))
+__global__ void synth_kernel(uint64_t seed, uint32_t stream, uint64_t n, int kind, double div,
+                             uint16_t* out16, float* out32, int64_t rows, int64_t cols,
+                             int transpose) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint16_t hb = f64_to_f16_bits(synth_value(kind, uniform(seed, stream, i), div));
+    uint64_t idx = i;
+    if (transpose) idx = (i % (uint64_t)cols) * (uint64_t)rows + i / (uint64_t)cols;
+    if (out16) out16[idx] = hb;
+    else out32[idx] = f16_bits_to_f32(hb);
+  }
+}
+
+// KV prefix [H][count][d] -> cache [H][max_seq][d]
+__global__ void kv_synth_kernel(uint64_t seed, uint32_t stream, int H, int count, int d, int max_seq,
+                                uint16_t* out) {
+  const uint64_t n = (uint64_t)H * count * d;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t hh = i / ((uint64_t)count * d), rem = i % ((uint64_t)count * d);
+    out[hh * (uint64_t)max_seq * d + rem] = f64_to_f16_bits(synth_value(K_KV, uniform(seed, stream, i), 1.0));
+  }
+}
+
+int launch_synth(cudaStream_t st, uint64_t seed, uint32_t stream, uint64_t n, int kind, double div,
+                 uint16_t* out16, float* out32, int64_t rows = 0, int64_t cols = 0, int transpose = 0) {
+  const int block = 256;
+  const uint64_t want = (n + block - 1) / block;
+  const int grid = (int)std::min<uint64_t>(want, 148 * 32);
+  synth_kernel<<<std::max(grid, 1), block, 0, st>>>(seed, stream, n, kind, div, out16, out32, rows,
+                                                    cols, transpose);
+  CK(cudaGetLastError());
+  return NFB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// Context
+// ===========================================================================
+struct LayerBufs {
+  uint16_t *wqkv = nullptr, *woT = nullptr, *wup = nullptr, *wdT = nullptr, *kc = nullptr, *vc = nullptr;
+  float *bqkv = nullptr, *bo = nullptr, *bup = nullptr, *bd = nullptr;
+  float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
+  bool weights = false;
+  int kv_len = 0;
+};
+
+struct nfb_ctx {
+  nfb_model_desc desc{};
+  int device = 0;
+  int max_seq = 0;
+  int C = 2, n_clusters = 0, grid = 0, ncw = 0, block = 0, dpl = 16;
+  int stage_rows = 8, slot_bytes = 0, n_slots = 0, kv_pos = 0, smem = 0, sm_count = 0;
+  bool coop = true;
+  cudaStream_t stream = nullptr;
+  std::vector<LayerBufs> layers;
+  LayerW* d_layers = nullptr;
+  uint16_t *embed = nullptr, *unembed = nullptr;
+  float *lnfg = nullptr, *lnfb = nullptr;
+  bool has_embed = false, has_unembed = false, has_lnf = false;
+  float2* rope = nullptr;
+  float *xs = nullptr, *rbuf = nullptr, *part = nullptr, *logits = nullptr;
+  int *ctr = nullptr, *state = nullptr, *tokens = nullptr, *err = nullptr;
+  unsigned* gbar = nullptr;
+  unsigned long long* amax = nullptr;
+  int ctr_stride = 0;
+  // pinned staging
+  float *h_x = nullptr, *h_hidden = nullptr, *h_logits = nullptr;
+  int* h_state = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int decode_pos = -1;  // host mirror of the device position in decode mode
+  int decode_step = 0;  // host mirror of the device step counter
+  unsigned long long* h_tok = nullptr;  // pinned [2]
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+template <class T>
+int dalloc(nfb_ctx* c, T** p, size_t n) {
+  void* q = nullptr;
+  CK(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)));
+  CK(cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(T)));
+  c->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return NFB_OK;
+}
+
+#define TRY(expr)              \
+  do {                         \
+    int r_ = (expr);           \
+    if (r_ != NFB_OK) return r_; \
+  } while (0)
+
+Params base_params(nfb_ctx* c) {
+  Params p{};
+  const nfb_model_desc& m = c->desc;
+  p.h = m.hidden;
+  p.H = m.n_heads;
+  p.d = m.d_head;
+  p.m = m.d_mlp;
+  p.rd = m.rotary_dims;
+  p.V = m.vocab;
+  p.max_seq = c->max_seq;
+  p.eps = (float)m.ln_eps;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m.d_head));
+  p.parallel = m.parallel_residual ? 1 : 0;
+  p.gelu_exact = m.gelu_exact ? 1 : 0;
+  p.C = c->C;
+  p.n_clusters = c->n_clusters;
+  p.ncw = c->ncw;
+  p.rows_qkv = 3 * m.d_head / c->C;
+  p.rows_o = m.d_head / c->C;
+  p.stage_rows = c->stage_rows;
+  p.n_slots = c->n_slots;
+  p.slot_bytes = c->slot_bytes;
+  p.kv_pos = c->kv_pos;
+  p.layers = c->d_layers;
+  p.head.embed = reinterpret_cast<const __half*>(c->embed);
+  p.head.lnfg = c->lnfg;
+  p.head.lnfb = c->lnfb;
+  p.head.unembed = reinterpret_cast<const __half*>(c->unembed);
+  p.rope = c->rope;
+  p.xs = c->xs;
+  p.rbuf = c->rbuf;
+  p.part = c->part;
+  p.ctr = c->ctr;
+  p.ctr_stride = c->ctr_stride;
+  p.gbar = c->gbar;
+  p.state = c->state;
+  p.amax = c->amax;
+  p.tokens = c->tokens;
+  p.logits = c->logits;
+  p.err = c->err;
+  return p;
+}
+
+int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {
+  cudaError_t e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, st, c->coop);
+  if (e != cudaSuccess && c->coop) {
+    // Cooperative + cluster launch refused: fall back to the occupancy-checked
+    // plain cluster launch (grid <= max active clusters, one CTA per SM).
+    cudaGetLastError();
+    c->coop = false;
+    e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, st, false);
+  }
+  if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+  return NFB_OK;
+}
+
+int check_device_error(nfb_ctx* c) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    int code = 0;
+    cudaMemcpy(&code, c->err, sizeof(int), cudaMemcpyDeviceToHost);
+    return fail(NFB_EDEVICE, std::string("device failure (watchdog code ") + std::to_string(code) +
+                                 "): " + cudaGetErrorString(e));
+  }
+  return NFB_OK;
+}
+
+int to_f16_host(const void* src, int dtype, size_t n, std::vector<uint16_t>& out) {
+  out.resize(n);
+  if (dtype == NFB_F64) {
+    const double* s = static_cast<const double*>(src);
+    for (size_t i = 0; i < n; ++i) out[i] = f64_to_f16_bits(s[i]);
+  } else if (dtype == NFB_F32) {
+    const float* s = static_cast<const float*>(src);
+    for (size_t i = 0; i < n; ++i) out[i] = f64_to_f16_bits((double)s[i]);
+  } else if (dtype == NFB_F16) {
+    memcpy(out.data(), src, n * 2);
+  } else {
+    return fail(NFB_EINVAL, "dtype must be NFB_F64, NFB_F32 or NFB_F16");
+  }
+  return NFB_OK;
+}
+
+int upload_f16(const void* src, int dtype, size_t rows, size_t cols, bool transpose, uint16_t* dst) {
+  std::vector<uint16_t> h;
+  TRY(to_f16_host(src, dtype, rows * cols, h));
+  if (transpose) {
+    std::vector<uint16_t> t(rows * cols);
+    for (size_t r = 0; r < rows; ++r)
+      for (size_t k = 0; k < cols; ++k) t[k * rows + r] = h[r * cols + k];
+    h.swap(t);
+  }
+  CK(cudaMemcpy(dst, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  return NFB_OK;
+}
+
+int upload_f32_of_f16(const void* src, int dtype, size_t n, float* dst) {
+  std::vector<uint16_t> h;
+  TRY(to_f16_host(src, dtype, n, h));
+  std::vector<float> f(n);
+  for (size_t i = 0; i < n; ++i) f[i] = f16_bits_to_f32(h[i]);
+  CK(cudaMemcpy(dst, f.data(), n * 4, cudaMemcpyHostToDevice));
+  return NFB_OK;
+}
+
+int check_layer(nfb_ctx* c, int layer) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (layer < 0 || layer >= c->desc.n_layers)
+    return fail(NFB_EINVAL, "layer " + std::to_string(layer) + " out of range");
+  return NFB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int nfb_version(void) { return 100; }
+
+const char* nfb_last_error(void) { return g_err.c_str(); }
+
+int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_size,
+               int max_clusters, nfb_ctx** out) {
+  if (!desc || !out) return fail(NFB_EINVAL, "null argument");
+  *out = nullptr;
+  const nfb_model_desc& m = *desc;
+  if (m.hidden < 1 || m.n_heads < 1 || m.d_head < 1 || m.n_layers < 1 || m.d_mlp < 1 || m.vocab < 1)
+    return fail(NFB_EINVAL, "model dimensions must be >= 1");
+  if (m.hidden != m.n_heads * m.d_head)
+    return fail(NFB_EINVAL, "hidden (" + std::to_string(m.hidden) + ") must equal n_heads * d_head (" +
+                                std::to_string(m.n_heads) + " * " + std::to_string(m.d_head) + ")");
+  if (m.rotary_dims < 2 || m.rotary_dims % 2 || m.rotary_dims > m.d_head)
+    return fail(NFB_EINVAL, "rotary_dims must be an even number >= 2 and <= d_head");
+  if (!(m.ln_eps > 0.0)) return fail(NFB_EINVAL, "ln_eps must be positive");
+  if (m.hidden % 8 || m.hidden > 32 * 8 * kMaxConsumerWarps)
+    return fail(NFB_EUNSUPPORTED, "hidden must be a multiple of 8 and <= 4096");
+  if (m.d_head % 8) return fail(NFB_EUNSUPPORTED, "d_head must be a multiple of 8");
+  if (max_seq < 1) return fail(NFB_EINVAL, "max_seq must be >= 1");
+  const int C = cluster_size > 0 ? cluster_size : 2;
+  if (C > 8 || (3 * m.d_head) % C || m.d_head % C)
+    return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8 and divide d_head");
+
+  nfb_ctx* c = new nfb_ctx();
+  c->desc = m;
+  c->device = device;
+  c->max_seq = max_seq;
+  c->C = C;
+  auto bail = [&](int code) {
+    nfb_destroy(c);
+    return code;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(fail(NFB_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(fail(NFB_ECUDA, cudaGetErrorString(e)));
+
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  c->sm_count = prop.multiProcessorCount;
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+
+  c->ncw = (m.hidden / 8 + 31) / 32;
+  c->block = (c->ncw + 1) * 32;
+  c->dpl = c->block <= 384 ? 0 : 1;  // kernel variant (max threads per block)
+  c->stage_rows = m.hidden >= 4096 ? 4 : kRows;
+  c->slot_bytes = std::max(c->stage_rows * m.hidden * 2, 4 * m.d_head * 2 * 2);
+  c->kv_pos = c->slot_bytes / (4 * m.d_head);
+  Params probe = base_params(c);
+  probe.n_slots = 0;
+  const int fixed = make_layout(probe).total;
+  const int per_slot = c->slot_bytes + 32;
+  c->n_slots = std::min(12, (smem_optin - fixed - 128) / per_slot);
+  if (c->n_slots < 2) return bail(fail(NFB_EUNSUPPORTED, "shared memory too small for the stage ring"));
+  probe.n_slots = c->n_slots;
+  c->smem = make_layout(probe).total;
+
+  e = cudaFuncSetAttribute(decode_kernel_ptr(c->dpl), cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem);
+  if (e != cudaSuccess) return bail(fail(NFB_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e)));
+  int nc = 0;
+  e = max_active_clusters(c->dpl, C, c->block, c->smem, &nc);
+  if (e != cudaSuccess || nc < 1)
+    return bail(fail(NFB_ECUDA, std::string("no co-resident cluster fits: ") + cudaGetErrorString(e)));
+  if (max_clusters > 0) nc = std::min(nc, max_clusters);
+  c->n_clusters = nc;
+  c->grid = nc * C;
+
+  const int L = m.n_layers, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
+  c->layers.resize(L);
+  std::vector<LayerW> table(L);
+  for (int l = 0; l < L; ++l) {
+    LayerBufs& b = c->layers[l];
+    int r = NFB_OK;
+    if ((r = dalloc(c, &b.wqkv, (size_t)3 * h * h)) || (r = dalloc(c, &b.woT, (size_t)h * h)) ||
+        (r = dalloc(c, &b.wup, (size_t)mm * h)) || (r = dalloc(c, &b.wdT, (size_t)mm * h)) ||
+        (r = dalloc(c, &b.bqkv, (size_t)3 * h)) || (r = dalloc(c, &b.bo, h)) ||
+        (r = dalloc(c, &b.bup, mm)) || (r = dalloc(c, &b.bd, h)) || (r = dalloc(c, &b.ln1g, h)) ||
+        (r = dalloc(c, &b.ln1b, h)) || (r = dalloc(c, &b.ln2g, h)) || (r = dalloc(c, &b.ln2b, h)) ||
+        (r = dalloc(c, &b.kc, (size_t)H * max_seq * d)) || (r = dalloc(c, &b.vc, (size_t)H * max_seq * d)))
+      return bail(r);
+    LayerW& w = table[l];
+    w.wqkv = reinterpret_cast<const __half*>(b.wqkv);
+    w.woT = reinterpret_cast<const __half*>(b.woT);
+    w.wup = reinterpret_cast<const __half*>(b.wup);
+    w.wdT = reinterpret_cast<const __half*>(b.wdT);
+    w.bqkv = b.bqkv;
+    w.bo = b.bo;
+    w.bup = b.bup;
+    w.bd = b.bd;
+    w.ln1g = b.ln1g;
+    w.ln1b = b.ln1b;
+    w.ln2g = b.ln2g;
+    w.ln2b = b.ln2b;
+    w.kc = reinterpret_cast<__half*>(b.kc);
+    w.vc = reinterpret_cast<__half*>(b.vc);
+  }
+  int r = NFB_OK;
+  c->ctr_stride = L + 2;
+  if ((r = dalloc(c, &c->d_layers, L)) || (r = dalloc(c, &c->embed, (size_t)V * h)) ||
+      (r = dalloc(c, &c->unembed, (size_t)V * h)) || (r = dalloc(c, &c->lnfg, h)) ||
+      (r = dalloc(c, &c->lnfb, h)) || (r = dalloc(c, &c->rope, (size_t)max_seq * (m.rotary_dims / 2))) ||
+      (r = dalloc(c, &c->xs, (size_t)(L + 1) * h)) || (r = dalloc(c, &c->rbuf, h)) ||
+      (r = dalloc(c, &c->part, (size_t)nc * h)) || (r = dalloc(c, &c->logits, V)) ||
+      (r = dalloc(c, &c->ctr, 2 * c->ctr_stride)) || (r = dalloc(c, &c->gbar, 2)) ||
+      (r = dalloc(c, &c->state, 2)) || (r = dalloc(c, &c->amax, 2)) ||
+      (r = dalloc(c, &c->tokens, max_seq)) || (r = dalloc(c, &c->err, 1)))
+    return bail(r);
+  e = cudaMemcpy(c->d_layers, table.data(), sizeof(LayerW) * L, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return bail(fail(NFB_ECUDA, cudaGetErrorString(e)));
+
+  // RoPE table: angle = pos * base^(-2i/rd) in f64 (nf/golden.py:68-71), cos/sin -> fp32
+  const int half = m.rotary_dims / 2;
+  std::vector<float2> rope((size_t)max_seq * half);
+  for (int pos = 0; pos < max_seq; ++pos)
+    for (int i = 0; i < half; ++i) {
+      const double th = pos * std::pow(m.theta_base, -2.0 * i / m.rotary_dims);
+      rope[(size_t)pos * half + i] = make_float2((float)std::cos(th), (float)std::sin(th));
+    }
+  e = cudaMemcpy(c->rope, rope.data(), rope.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return bail(fail(NFB_ECUDA, cudaGetErrorString(e)));
+
+  if (cudaMallocHost(&c->h_x, (size_t)h * 4) != cudaSuccess ||
+      cudaMallocHost(&c->h_hidden, (size_t)(L + 1) * h * 4) != cudaSuccess ||
+      cudaMallocHost(&c->h_logits, (size_t)V * 4) != cudaSuccess ||
+      cudaMallocHost(&c->h_state, 4 * sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&c->h_tok, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(NFB_ECUDA, "pinned host staging allocation failed"));
+  *out = c;
+  return NFB_OK;
+}
+
+int nfb_destroy(nfb_ctx* c) {
+  if (!c) return NFB_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->h_x) cudaFreeHost(c->h_x);
+  if (c->h_hidden) cudaFreeHost(c->h_hidden);
+  if (c->h_logits) cudaFreeHost(c->h_logits);
+  if (c->h_state) cudaFreeHost(c->h_state);
+  if (c->h_tok) cudaFreeHost(c->h_tok);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return NFB_OK;
+}
+
+int nfb_get_info(nfb_ctx* c, nfb_info* info) {
+  if (!c || !info) return fail(NFB_EINVAL, "null argument");
+  info->grid = c->grid;
+  info->cluster_size = c->C;
+  info->n_clusters = c->n_clusters;
+  info->consumer_warps = c->ncw;
+  info->stage_rows = c->stage_rows;
+  info->n_slots = c->n_slots;
+  info->slot_bytes = c->slot_bytes;
+  info->kv_stage_pos = c->kv_pos;
+  info->smem_bytes = c->smem;
+  info->max_seq = c->max_seq;
+  info->sm_count = c->sm_count;
+  return NFB_OK;
+}
+
+void* nfb_stream(nfb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int nfb_set_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w, int dtype) {
+  TRY(check_layer(c, layer));
+  if (!w) return fail(NFB_EINVAL, "null weights");
+  const void* ptrs[12] = {w->ln1_gain, w->ln1_bias, w->qkv_weight, w->qkv_bias, w->out_weight, w->out_bias,
+                          w->ln2_gain, w->ln2_bias, w->up_weight, w->up_bias, w->down_weight, w->down_bias};
+  for (const void* p : ptrs)
+    if (!p) return fail(NFB_EINVAL, "every BlockWeights tensor is required");
+  cudaSetDevice(c->device);
+  const int h = c->desc.hidden, m = c->desc.d_mlp;
+  LayerBufs& b = c->layers[layer];
+  TRY(upload_f32_of_f16(w->ln1_gain, dtype, h, b.ln1g));
+  TRY(upload_f32_of_f16(w->ln1_bias, dtype, h, b.ln1b));
+  TRY(upload_f16(w->qkv_weight, dtype, (size_t)3 * h, h, false, b.wqkv));
+  TRY(upload_f32_of_f16(w->qkv_bias, dtype, (size_t)3 * h, b.bqkv));
+  TRY(upload_f16(w->out_weight, dtype, h, h, true, b.woT));
+  TRY(upload_f32_of_f16(w->out_bias, dtype, h, b.bo));
+  TRY(upload_f32_of_f16(w->ln2_gain, dtype, h, b.ln2g));
+  TRY(upload_f32_of_f16(w->ln2_bias, dtype, h, b.ln2b));
+  TRY(upload_f16(w->up_weight, dtype, m, h, false, b.wup));
+  TRY(upload_f32_of_f16(w->up_bias, dtype, m, b.bup));
+  TRY(upload_f16(w->down_weight, dtype, h, m, true, b.wdT));
+  TRY(upload_f32_of_f16(w->down_bias, dtype, h, b.bd));
+  b.weights = true;
+  return NFB_OK;
+}
+
+int nfb_synth_block_weights(nfb_ctx* c, int layer, uint64_t seed) {
+  TRY(check_layer(c, layer));
+  cudaSetDevice(c->device);
+  const int64_t h = c->desc.hidden, m = c->desc.d_mlp;
+  LayerBufs& b = c->layers[layer];
+  cudaStream_t st = c->stream;
+  // stream index = position in BlockWeights field order (nf/weights.py:55, 80-82)
+  TRY(launch_synth(st, seed, 0, h, K_GAIN, 1.0, nullptr, b.ln1g));
+  TRY(launch_synth(st, seed, 1, h, K_LNBIAS, 1.0, nullptr, b.ln1b));
+  TRY(launch_synth(st, seed, 2, 3 * h * h, K_WEIGHT, std::sqrt((double)h), b.wqkv, nullptr));
+  TRY(launch_synth(st, seed, 3, 3 * h, K_BIAS, 1.0, nullptr, b.bqkv));
+  TRY(launch_synth(st, seed, 4, h * h, K_WEIGHT, std::sqrt((double)h), b.woT, nullptr, h, h, 1));
+  TRY(launch_synth(st, seed, 5, h, K_BIAS, 1.0, nullptr, b.bo));
+  TRY(launch_synth(st, seed, 6, h, K_GAIN, 1.0, nullptr, b.ln2g));
+  TRY(launch_synth(st, seed, 7, h, K_LNBIAS, 1.0, nullptr, b.ln2b));
+  TRY(launch_synth(st, seed, 8, m * h, K_WEIGHT, std::sqrt((double)h), b.wup, nullptr));
+  TRY(launch_synth(st, seed, 9, m, K_BIAS, 1.0, nullptr, b.bup));
+  TRY(launch_synth(st, seed, 10, h * m, K_WEIGHT, std::sqrt((double)m), b.wdT, nullptr, h, m, 1));
+  TRY(launch_synth(st, seed, 11, h, K_BIAS, 1.0, nullptr, b.bd));
+  CK(cudaStreamSynchronize(st));
+  b.weights = true;
+  return NFB_OK;
+}
+
+static int read_f16(const uint16_t* src, size_t rows, size_t cols, bool transpose, void* dst) {
+  std::vector<uint16_t> h(rows * cols);
+  CK(cudaMemcpy(h.data(), src, h.size() * 2, cudaMemcpyDeviceToHost));
+  float* o = static_cast<float*>(dst);
+  for (size_t r = 0; r < rows; ++r)
+    for (size_t k = 0; k < cols; ++k)
+      o[r * cols + k] = f16_bits_to_f32(transpose ? h[k * rows + r] : h[r * cols + k]);
+  return NFB_OK;
+}
+
+static int read_f32(const float* src, size_t n, void* dst) {
+  CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+int nfb_read_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w) {
+  TRY(check_layer(c, layer));
+  if (!w) return fail(NFB_EINVAL, "null weights");
+  cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
+  const size_t h = c->desc.hidden, m = c->desc.d_mlp;
+  LayerBufs& b = c->layers[layer];
+  void* o[12] = {(void*)w->ln1_gain, (void*)w->ln1_bias, (void*)w->qkv_weight, (void*)w->qkv_bias,
+                 (void*)w->out_weight, (void*)w->out_bias, (void*)w->ln2_gain, (void*)w->ln2_bias,
+                 (void*)w->up_weight, (void*)w->up_bias, (void*)w->down_weight, (void*)w->down_bias};
+  for (void* p : o)
+    if (!p) return fail(NFB_EINVAL, "every output tensor is required");
+  TRY(read_f32(b.ln1g, h, o[0]));
+  TRY(read_f32(b.ln1b, h, o[1]));
+  TRY(read_f16(b.wqkv, 3 * h, h, false, o[2]));
+  TRY(read_f32(b.bqkv, 3 * h, o[3]));
+  TRY(read_f16(b.woT, h, h, true, o[4]));
+  TRY(read_f32(b.bo, h, o[5]));
+  TRY(read_f32(b.ln2g, h, o[6]));
+  TRY(read_f32(b.ln2b, h, o[7]));
+  TRY(read_f16(b.wup, m, h, false, o[8]));
+  TRY(read_f32(b.bup, m, o[9]));
+  TRY(read_f16(b.wdT, h, m, true, o[10]));
+  TRY(read_f32(b.bd, h, o[11]));
+  return NFB_OK;
+}
+
+int nfb_set_head(nfb_ctx* c, const void* embed, const void* lnf_gain, const void* lnf_bias,
+                 const void* unembed, int dtype) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  cudaSetDevice(c->device);
+  const size_t h = c->desc.hidden, V = c->desc.vocab;
+  if (embed) {
+    TRY(upload_f16(embed, dtype, V, h, false, c->embed));
+    c->has_embed = true;
+  }
+  if (lnf_gain || lnf_bias) {
+    if (!lnf_gain || !lnf_bias) return fail(NFB_EINVAL, "final LN needs gain and bias");
+    TRY(upload_f32_of_f16(lnf_gain, dtype, h, c->lnfg));
+    TRY(upload_f32_of_f16(lnf_bias, dtype, h, c->lnfb));
+    c->has_lnf = true;
+  }
+  if (unembed) {
+    TRY(upload_f16(unembed, dtype, V, h, false, c->unembed));
+    c->has_unembed = true;
+  }
+  return NFB_OK;
+}
+
+int nfb_synth_head(nfb_ctx* c, uint64_t seed) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  cudaSetDevice(c->device);
+  const int64_t h = c->desc.hidden, V = c->desc.vocab;
+  cudaStream_t st = c->stream;
+  TRY(launch_synth(st, seed, 0, V * h, K_PLAIN, 1.0, c->embed, nullptr));
+  TRY(launch_synth(st, seed, 1, h, K_GAIN, 1.0, nullptr, c->lnfg));
+  TRY(launch_synth(st, seed, 2, h, K_LNBIAS, 1.0, nullptr, c->lnfb));
+  TRY(launch_synth(st, seed, 3, V * h, K_WEIGHT, std::sqrt((double)h), c->unembed, nullptr));
+  CK(cudaStreamSynchronize(st));
+  c->has_embed = c->has_lnf = c->has_unembed = true;
+  return NFB_OK;
+}
+
+int nfb_kv_write(nfb_ctx* c, int layer, int start, int count, const void* keys, const void* values,
+                 int dtype) {
+  TRY(check_layer(c, layer));
+  LayerBufs& b = c->layers[layer];
+  if (start < 0 || count < 0 || start > b.kv_len || start + count > c->max_seq)
+    return fail(NFB_EINVAL, "KV write range [" + std::to_string(start) + ", " + std::to_string(start + count) +
+                                ") invalid for a cache holding " + std::to_string(b.kv_len) +
+                                " positions (capacity " + std::to_string(c->max_seq) + ")");
+  if (count && (!keys || !values)) return fail(NFB_EINVAL, "null keys/values");
+  cudaSetDevice(c->device);
+  const size_t H = c->desc.n_heads, d = c->desc.d_head;
+  if (count) {
+    std::vector<uint16_t> hk, hv;
+    TRY(to_f16_host(keys, dtype, H * count * d, hk));
+    TRY(to_f16_host(values, dtype, H * count * d, hv));
+    CK(cudaMemcpy2D(b.kc + (size_t)start * d, c->max_seq * d * 2, hk.data(), (size_t)count * d * 2,
+                    (size_t)count * d * 2, H, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(b.vc + (size_t)start * d, c->max_seq * d * 2, hv.data(), (size_t)count * d * 2,
+                    (size_t)count * d * 2, H, cudaMemcpyHostToDevice));
+  }
+  b.kv_len = start + count;
+  return NFB_OK;
+}
+
+int nfb_kv_read(nfb_ctx* c, int layer, int start, int count, float* keys, float* values) {
+  TRY(check_layer(c, layer));
+  LayerBufs& b = c->layers[layer];
+  if (start < 0 || count < 0 || start + count > c->max_seq) return fail(NFB_EINVAL, "KV read range invalid");
+  cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
+  const size_t H = c->desc.n_heads, d = c->desc.d_head;
+  std::vector<uint16_t> hk(H * count * d), hv(H * count * d);
+  if (count) {
+    CK(cudaMemcpy2D(hk.data(), (size_t)count * d * 2, b.kc + (size_t)start * d, c->max_seq * d * 2,
+                    (size_t)count * d * 2, H, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy2D(hv.data(), (size_t)count * d * 2, b.vc + (size_t)start * d, c->max_seq * d * 2,
+                    (size_t)count * d * 2, H, cudaMemcpyDeviceToHost));
+  }
+  for (size_t i = 0; i < hk.size(); ++i) {
+    if (keys) keys[i] = f16_bits_to_f32(hk[i]);
+    if (values) values[i] = f16_bits_to_f32(hv[i]);
+  }
+  return NFB_OK;
+}
+
+int nfb_kv_synth(nfb_ctx* c, int layer, int count, uint64_t seed) {
+  TRY(check_layer(c, layer));
+  if (count < 0 || count > c->max_seq) return fail(NFB_EINVAL, "KV synth count out of range");
+  cudaSetDevice(c->device);
+  LayerBufs& b = c->layers[layer];
+  const int H = c->desc.n_heads, d = c->desc.d_head;
+  if (count) {
+    const int grid = 148 * 8;
+    kv_synth_kernel<<<grid, 256, 0, c->stream>>>(seed, 0, H, count, d, c->max_seq, b.kc);
+    kv_synth_kernel<<<grid, 256, 0, c->stream>>>(seed, 1, H, count, d, c->max_seq, b.vc);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  b.kv_len = count;
+  return NFB_OK;
+}
+
+static int check_ready(nfb_ctx* c, int l0, int l1, int pos, bool rewind = false) {
+  for (int l = l0; l < l1; ++l) {
+    const LayerBufs& b = c->layers[l];
+    if (!b.weights) return fail(NFB_ESTATE, "weights of layer " + std::to_string(l) + " not set");
+    if (b.kv_len != pos && !(rewind && pos <= b.kv_len))
+      return fail(NFB_EINVAL, "cache holds " + std::to_string(b.kv_len) + " positions, expected " +
+                                  std::to_string(pos));
+  }
+  if (pos < 0 || pos + 1 > c->max_seq)
+    return fail(NFB_EINVAL, "position " + std::to_string(pos) + " exceeds KV capacity " +
+                                std::to_string(c->max_seq));
+  return NFB_OK;
+}
+
+static int check_finite(const float* x, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return fail(NFB_EINVAL, "non-finite activation");
+  return NFB_OK;
+}
+
+int nfb_block_step(nfb_ctx* c, int layer, int pos, const float* x_in, float* x_out) {
+  TRY(check_layer(c, layer));
+  if (!x_in || !x_out) return fail(NFB_EINVAL, "null x");
+  TRY(check_ready(c, layer, layer + 1, pos));
+  TRY(check_finite(x_in, c->desc.hidden));
+  cudaSetDevice(c->device);
+  const int h = c->desc.hidden;
+  memcpy(c->h_x, x_in, (size_t)h * 4);
+  c->h_state[0] = pos;
+  CK(cudaMemcpyAsync(c->xs, c->h_x, (size_t)h * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->state, c->h_state, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  Params p = base_params(c);
+  p.l0 = layer;
+  p.l1 = layer + 1;
+  p.in_mode = IN_X;
+  p.head_mode = HEAD_NONE;
+  p.advance_pos = 0;
+  TRY(launch(c, p, c->stream));
+  CK(cudaMemcpyAsync(c->h_hidden, c->xs + h, (size_t)h * 4, cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_device_error(c));
+  memcpy(x_out, c->h_hidden, (size_t)h * 4);
+  c->layers[layer].kv_len = pos + 1;
+  c->decode_pos = -1;
+  return NFB_OK;
+}
+
+int nfb_forward(nfb_ctx* c, int pos, const float* x_in, float* hidden_out, float* logits_out,
+                int head_mode) {
+  if (!c || !x_in) return fail(NFB_EINVAL, "null argument");
+  const int L = c->desc.n_layers, h = c->desc.hidden, V = c->desc.vocab;
+  TRY(check_ready(c, 0, L, pos));
+  TRY(check_finite(x_in, h));
+  if (head_mode < NFB_HEAD_NONE || head_mode > NFB_HEAD_LM) return fail(NFB_EINVAL, "bad head_mode");
+  if (head_mode != NFB_HEAD_NONE && !c->has_unembed) return fail(NFB_ESTATE, "unembedding not set");
+  if (head_mode == NFB_HEAD_LM && !c->has_lnf) return fail(NFB_ESTATE, "final LN not set");
+  cudaSetDevice(c->device);
+  memcpy(c->h_x, x_in, (size_t)h * 4);
+  c->h_state[0] = pos;
+  CK(cudaMemcpyAsync(c->xs, c->h_x, (size_t)h * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->state, c->h_state, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  Params p = base_params(c);
+  p.l0 = 0;
+  p.l1 = L;
+  p.in_mode = IN_X;
+  p.head_mode = head_mode;
+  p.advance_pos = 0;
+  TRY(launch(c, p, c->stream));
+  if (hidden_out)
+    CK(cudaMemcpyAsync(c->h_hidden, c->xs, (size_t)(L + 1) * h * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (logits_out && head_mode != NFB_HEAD_NONE)
+    CK(cudaMemcpyAsync(c->h_logits, c->logits, (size_t)V * 4, cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_device_error(c));
+  if (hidden_out) memcpy(hidden_out, c->h_hidden, (size_t)(L + 1) * h * 4);
+  if (logits_out && head_mode != NFB_HEAD_NONE) memcpy(logits_out, c->h_logits, (size_t)V * 4);
+  for (int l = 0; l < L; ++l) c->layers[l].kv_len = pos + 1;
+  c->decode_pos = -1;
+  return NFB_OK;
+}
+
+int nfb_begin_decode(nfb_ctx* c, int pos, int token) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  const int L = c->desc.n_layers;
+  TRY(check_ready(c, 0, L, pos, true));  // may rewind: positions >= pos are discarded
+  if (!c->has_embed || !c->has_unembed || !c->has_lnf) return fail(NFB_ESTATE, "embedding / LM head not set");
+  if (token < 0 || token >= c->desc.vocab) return fail(NFB_EINVAL, "token out of range");
+  cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
+  int st[2] = {pos, 0};
+  CK(cudaMemcpy(c->state, st, sizeof(st), cudaMemcpyHostToDevice));
+  unsigned long long am[2] = {0ull, (0xffffffffull << 32) | (unsigned long long)(0xffffffffu - (uint32_t)token)};
+  CK(cudaMemcpy(c->amax, am, sizeof(am), cudaMemcpyHostToDevice));
+  c->decode_pos = pos;
+  c->decode_step = 0;
+  for (auto& b : c->layers) b.kv_len = pos;
+  return NFB_OK;
+}
+
+static Params decode_params(nfb_ctx* c) {
+  Params p = base_params(c);
+  p.l0 = 0;
+  p.l1 = c->desc.n_layers;
+  p.in_mode = IN_TOKEN;
+  p.head_mode = HEAD_LM;
+  p.advance_pos = 1;
+  return p;
+}
+
+static int advance_host(nfb_ctx* c, int n) {
+  if (c->decode_pos < 0) return fail(NFB_ESTATE, "call nfb_begin_decode first");
+  if (c->decode_pos + n > c->max_seq) return fail(NFB_EINVAL, "decode would exceed the KV capacity");
+  return NFB_OK;
+}
+
+int nfb_decode_step(nfb_ctx* c, void* stream) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  TRY(advance_host(c, 1));
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  TRY(launch(c, decode_params(c), st));
+  c->decode_pos += 1;
+  c->decode_step += 1;
+  for (auto& b : c->layers) b.kv_len = c->decode_pos;
+  return NFB_OK;
+}
+
+int nfb_graph_capture(nfb_ctx* c) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  cudaSetDevice(c->device);
+  if (c->gexec) {
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+  }
+  if (c->graph) {
+    cudaGraphDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  // Resolve the cooperative fallback outside capture (a refused launch would
+  // invalidate the capture).
+  CK(cudaStreamSynchronize(c->stream));
+  const Params p = decode_params(c);
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, c->stream, c->coop);
+  cudaGraph_t g = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+  if ((e != cudaSuccess || e2 != cudaSuccess) && c->coop) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    c->coop = false;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, c->stream, false);
+    e2 = cudaStreamEndCapture(c->stream, &g);
+  }
+  if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("capture launch: ") + cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("end capture: ") + cudaGetErrorString(e2));
+  c->graph = g;
+  CK(cudaGraphInstantiate(&c->gexec, g, 0));
+  return NFB_OK;
+}
+
+int nfb_graph_replay(nfb_ctx* c, int n, void* stream) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (!c->gexec) return fail(NFB_ESTATE, "call nfb_graph_capture first");
+  if (n < 0) return fail(NFB_EINVAL, "n must be >= 0");
+  TRY(advance_host(c, n));
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  for (int i = 0; i < n; ++i) CK(cudaGraphLaunch(c->gexec, st));
+  c->decode_pos += n;
+  c->decode_step += n;
+  for (auto& b : c->layers) b.kv_len = c->decode_pos;
+  return NFB_OK;
+}
+
+int nfb_step_token(nfb_ctx* c, int token, int* next_token) {
+  if (!c || !next_token) return fail(NFB_EINVAL, "null argument");
+  if (token < 0 || token >= c->desc.vocab) return fail(NFB_EINVAL, "token out of range");
+  TRY(advance_host(c, 1));
+  cudaSetDevice(c->device);
+  const int par = c->decode_step & 1;
+  // the step reads its input token from slot par^1 and writes its argmax to slot par
+  c->h_tok[0] = (0xffffffffull << 32) | (unsigned long long)(0xffffffffu - (uint32_t)token);
+  CK(cudaMemcpyAsync(c->amax + (par ^ 1), c->h_tok, 8, cudaMemcpyHostToDevice, c->stream));
+  if (c->gexec) {
+    CK(cudaGraphLaunch(c->gexec, c->stream));
+  } else {
+    TRY(launch(c, decode_params(c), c->stream));
+  }
+  CK(cudaMemcpyAsync(c->h_tok + 1, c->amax + par, 8, cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_device_error(c));
+  c->decode_pos += 1;
+  c->decode_step += 1;
+  for (auto& b : c->layers) b.kv_len = c->decode_pos;
+  *next_token = (int)(0xffffffffu - (uint32_t)(c->h_tok[1] & 0xffffffffull));
+  return NFB_OK;
+}
+
+int nfb_sync(nfb_ctx* c) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  cudaSetDevice(c->device);
+  return check_device_error(c);
+}
+
+int nfb_get_state(nfb_ctx* c, int* pos, int* step) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  TRY(nfb_sync(c));
+  int st[2];
+  CK(cudaMemcpy(st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
+  if (pos) *pos = st[0];
+  if (step) *step = st[1];
+  return NFB_OK;
+}
+
+int nfb_read_tokens(nfb_ctx* c, int* tokens, int n, int* last_argmax) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (n < 0 || n > c->max_seq) return fail(NFB_EINVAL, "n out of range");
+  TRY(nfb_sync(c));
+  if (tokens && n) CK(cudaMemcpy(tokens, c->tokens, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost));
+  if (last_argmax) {
+    int st[2];
+    CK(cudaMemcpy(st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
+    unsigned long long am[2];
+    CK(cudaMemcpy(am, c->amax, sizeof(am), cudaMemcpyDeviceToHost));
+    const unsigned long long v = am[(st[1] + 1) & 1];  // written by step st[1]-1
+    *last_argmax = (int)(0xffffffffu - (uint32_t)(v & 0xffffffffull));
+  }
+  return NFB_OK;
+}
+
+int nfb_read_hidden(nfb_ctx* c, float* out) {
+  if (!c || !out) return fail(NFB_EINVAL, "null argument");
+  TRY(nfb_sync(c));
+  CK(cudaMemcpy(out, c->xs, (size_t)(c->desc.n_layers + 1) * c->desc.hidden * 4, cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+int nfb_read_logits(nfb_ctx* c, float* out) {
+  if (!c || !out) return fail(NFB_EINVAL, "null argument");
+  TRY(nfb_sync(c));
+  CK(cudaMemcpy(out, c->logits, (size_t)c->desc.vocab * 4, cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,974 @@
+// Fused single-token GPT-NeoX decode step for sm_100a.
+//
+// One persistent, warp-specialised launch runs the fused decoder block for a
+// range of layers (plus, optionally, the LM / probe head).  Per CTA (one per
+// SM, grid = clusters of C CTAs):
+//   * warp `ncw` lane 0 is the PRODUCER: it walks the CTA's stage schedule and
+//     streams every weight row block and KV tile into a shared-memory ring with
+//     1-D bulk async copies (cp.async.bulk -> mbarrier complete_tx).  It never
+//     waits on activations, so HBM keeps streaming -- including the next
+//     layer's weights -- while consumers sit in cluster / grid rendezvous.
+//   * warps 0..ncw-1 are CONSUMERS.  Thread t owns hidden chunk t (8 elements)
+//     for everything: LN statistics, GEMV inputs and the split-K output
+//     partial, so row-dot products need one butterfly + one cross-warp sum and
+//     transposed projections (W_out^T, W_down^T) need no reduction at all.
+//
+// Reference semantics: nf/golden.py:189-228 (decoder_block_golden) and
+// nf/cluster.py:291-352 (fused_block_step).  Work split:
+//   * head h -> cluster h mod n_clusters.  Rank c of the cluster computes QKV
+//     rows [c*3d/C, (c+1)*3d/C) of the head, all ranks exchange them through
+//     DSMEM, each rank attends over its partition_kv() share of the history
+//     (nf/cluster.py:134-150) with the new token on the last rank, the C
+//     softmax states (m, l, o) are merged through DSMEM (nf/golden.py:128-136),
+//     and rank c applies W_out^T rows [c*d/C, (c+1)*d/C) of the head.
+//   * MLP rows (up row j + W_down^T row j) are grabbed dynamically by the
+//     producers of all CTAs from a per-layer counter.
+//   * layer end: DSMEM reduction of the C split-K partials to the cluster
+//     leader, then a deterministic fixed-order fold across clusters
+//     (grid barrier, per-CTA element slices, grid barrier).
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "nfb_internal.h"
+#include "nfb_ptx.cuh"
+
+namespace nfb {
+
+enum StageType : int {
+  ST_QKV = 1, ST_KV = 2, ST_WO = 3, ST_UP = 4, ST_DOWN = 5,
+  ST_SYNC = 6, ST_END = 7, ST_LM = 8, ST_HEAD_END = 9
+};
+constexpr int F_LAST = 1;
+
+struct Desc {
+  int type;
+  int a;      // first row / position
+  int n;      // rows / positions in this stage
+  int flags;  // bit 0: last stage of its group; bits 8..: head index
+};
+
+struct Smem {
+  unsigned char* ring;
+  uint64_t* full;
+  uint64_t* empty;
+  Desc* desc;
+  uint64_t* bar_qkv;
+  uint64_t* bar_att;
+  uint64_t* bar_red;
+  float* ybuf;
+  float* attst;
+  float* ctx;
+  float* wst;
+  float* wred;
+  float* red_in;
+  float* fold;
+  int* misc;
+  int attst_stride;
+  int wst_stride;
+};
+
+__device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, const Params& p) {
+  Smem s;
+  s.ring = base + L.ring;
+  s.full = reinterpret_cast<uint64_t*>(base + L.full);
+  s.empty = reinterpret_cast<uint64_t*>(base + L.empty);
+  s.desc = reinterpret_cast<Desc*>(base + L.desc);
+  s.bar_qkv = reinterpret_cast<uint64_t*>(base + L.bars);
+  s.bar_att = s.bar_qkv + 1;
+  s.bar_red = s.bar_qkv + 2;
+  s.ybuf = reinterpret_cast<float*>(base + L.ybuf);
+  s.attst = reinterpret_cast<float*>(base + L.attst);
+  s.ctx = reinterpret_cast<float*>(base + L.ctx);
+  s.wst = reinterpret_cast<float*>(base + L.wst);
+  s.wred = reinterpret_cast<float*>(base + L.wred);
+  s.red_in = reinterpret_cast<float*>(base + L.red_in);
+  s.fold = reinterpret_cast<float*>(base + L.fold);
+  s.misc = reinterpret_cast<int*>(base + L.misc);
+  s.attst_stride = align_up(p.d + 2, 4);
+  s.wst_stride = align_up(p.d + 2, 4);
+  return s;
+}
+
+// ===========================================================================
+// Producer
+// ===========================================================================
+struct Producer {
+  const Params& p;
+  const Smem& s;
+  uint32_t gs = 0;
+  uint64_t pol;
+
+  __device__ __forceinline__ Producer(const Params& p_, const Smem& s_) : p(p_), s(s_) { pol = policy_evict_first(); }
+
+  __device__ __forceinline__ void push(int type, int a, int n, int flags, const void* src0, uint32_t b0,
+                       const void* src1 = nullptr, uint32_t b1 = 0) {
+    const int slot = gs % p.n_slots;
+    const uint32_t ph = ((gs / p.n_slots) & 1u) ^ 1u;
+    mbar_wait(&s.empty[slot], ph, p.err, 10);
+    s.desc[slot] = Desc{type, a, n, flags};
+    const uint32_t bytes = b0 + b1;
+    unsigned char* dst = s.ring + (size_t)slot * p.slot_bytes;
+    if (bytes) {
+      mbar_arrive_expect_tx(&s.full[slot], bytes);
+      bulk_g2s(dst, src0, b0, &s.full[slot], pol);
+      if (b1) bulk_g2s(dst + b0, src1, b1, &s.full[slot], pol);
+    } else {
+      mbar_arrive(&s.full[slot]);
+    }
+    ++gs;
+  }
+
+  int mlp_c0 = 0, mlp_c1 = 0;
+
+  // Head-stage bytes of CTA (cluster k, rank r) at history length pos.
+  __device__ __forceinline__ long long head_bytes(int k, int r, int pos) const {
+    if (k >= p.H) return 0;
+    const int nh = (p.H - k + p.n_clusters - 1) / p.n_clusters;
+    const int cnt = pos / p.C + (r < pos % p.C ? 1 : 0);
+    return (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
+  }
+
+  // Static, byte-balanced MLP chunk ranges: every CTA evaluates the same
+  // formula, so the split-K partial of each CTA (and the fold) is bitwise
+  // reproducible run to run.  CTA g gets chunks [start_g, start_{g+1}) with
+  // start_g proportional to the prefix of max(0, T - headbytes_j).
+  __device__ __forceinline__ void mlp_range(int pos, uint32_t rank, uint32_t cid) {
+    const int G = p.n_clusters * p.C;
+    const long long n_ch = (p.m + p.stage_rows - 1) / p.stage_rows;
+    const long long chunk_b = 2ll * p.stage_rows * p.h * 2;
+    long long total = n_ch * chunk_b;
+    for (int g = 0; g < G; ++g) total += head_bytes(g / p.C, g % p.C, pos);
+    const long long T = total / G;
+    long long W = 0, cum = 0;
+    const int me = (int)(cid * p.C + rank);
+    for (int g = 0; g < G; ++g) {
+      const long long w = max(0ll, T - head_bytes(g / p.C, g % p.C, pos));
+      if (g == me) cum = W;
+      W += w;
+    }
+    const long long mine = max(0ll, T - head_bytes((int)cid, (int)rank, pos));
+    if (W <= 0) {
+      mlp_c0 = mlp_c1 = (me == 0) ? 0 : (int)n_ch;
+      if (me == 0) mlp_c1 = (int)n_ch;
+      return;
+    }
+    mlp_c0 = (int)(n_ch * cum / W);
+    mlp_c1 = (int)(n_ch * (cum + mine) / W);
+  }
+
+  __device__ __forceinline__ void run(int pos, int par, uint32_t rank, uint32_t cid) {
+    const int h = p.h, d = p.d, C = p.C;
+    const uint32_t rowb = (uint32_t)h * 2u;
+    if (!p.dyn_mlp) mlp_range(pos, rank, cid);
+    for (int l = p.l0; l < p.l1; ++l) {
+      const LayerW& W = p.layers[l];
+      const int lrel = l - p.l0;
+      for (int hh = (int)cid; hh < p.H; hh += p.n_clusters) {
+        const int tag = hh << 8;
+        // QKV rows of this head owned by this rank.
+        const int q0 = (int)rank * p.rows_qkv;
+        for (int r = 0; r < p.rows_qkv; r += p.stage_rows) {
+          const int n = min(p.stage_rows, p.rows_qkv - r);
+          const int last = (r + n >= p.rows_qkv) ? F_LAST : 0;
+          push(ST_QKV, q0 + r, n, tag | last, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h, n * rowb);
+        }
+        // KV history share (partition_kv: first hist % C ranks get one extra).
+        const int base = pos / C, extra = pos % C;
+        const int cnt = base + ((int)rank < extra ? 1 : 0);
+        const int st = (int)rank * base + min((int)rank, extra);
+        if (cnt == 0) push(ST_KV, st, 0, tag | F_LAST, nullptr, 0);
+        for (int q = 0; q < cnt; q += p.kv_pos) {
+          const int n = min(p.kv_pos, cnt - q);
+          const int last = (q + n >= cnt) ? F_LAST : 0;
+          const size_t off = ((size_t)hh * p.max_seq + st + q) * d;
+          push(ST_KV, st + q, n, tag | last, W.kc + off, (uint32_t)n * d * 2, W.vc + off,
+               (uint32_t)n * d * 2);
+        }
+        // W_out^T rows (context elements) owned by this rank.
+        const int o0 = (int)rank * p.rows_o;
+        for (int r = 0; r < p.rows_o; r += p.stage_rows) {
+          const int n = min(p.stage_rows, p.rows_o - r);
+          const int last = (r + n >= p.rows_o) ? F_LAST : 0;
+          push(ST_WO, o0 + r, n, tag | last, W.woT + (size_t)(hh * d + o0 + r) * h, n * rowb);
+        }
+      }
+      if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
+      if (p.dyn_mlp) {
+        int* ctr = p.ctr + par * p.ctr_stride + lrel;
+        for (;;) {
+          const int r = atomicAdd(ctr, 1) * p.stage_rows;
+          if (r >= p.m) break;
+          const int n = min(p.stage_rows, p.m - r);
+          push(ST_UP, r, n, 0, W.wup + (size_t)r * h, n * rowb);
+          push(ST_DOWN, r, n, 0, W.wdT + (size_t)r * h, n * rowb);
+        }
+      } else {
+        for (int c = mlp_c0; c < mlp_c1; ++c) {
+          const int r = c * p.stage_rows;
+          const int n = min(p.stage_rows, p.m - r);
+          push(ST_UP, r, n, 0, W.wup + (size_t)r * h, n * rowb);
+          push(ST_DOWN, r, n, 0, W.wdT + (size_t)r * h, n * rowb);
+        }
+      }
+      push(ST_END, 0, 0, 0, nullptr, 0);
+    }
+    if (p.head_mode != HEAD_NONE) {
+      int* ctr = p.ctr + par * p.ctr_stride + (p.l1 - p.l0);
+      for (;;) {
+        const int r = atomicAdd(ctr, 1) * p.stage_rows;
+        if (r >= p.V) break;
+        const int n = min(p.stage_rows, p.V - r);
+        push(ST_LM, r, n, 0, p.head.unembed + (size_t)r * h, n * rowb);
+      }
+      push(ST_HEAD_END, 0, 0, 0, nullptr, 0);
+    }
+  }
+};
+
+// ===========================================================================
+// Consumer helpers
+// ===========================================================================
+__device__ __forceinline__ void h8_to_f32(const uint4& w, float* f) {
+  const __half2* hp = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __half22float2(hp[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ float dot8(const uint4& w, const float* x) {
+  float f[8];
+  h8_to_f32(w, f);
+  float a = f[0] * x[0];
+  float b = f[1] * x[1];
+  a = fmaf(f[2], x[2], a);
+  b = fmaf(f[3], x[3], b);
+  a = fmaf(f[4], x[4], a);
+  b = fmaf(f[5], x[5], b);
+  a = fmaf(f[6], x[6], a);
+  b = fmaf(f[7], x[7], b);
+  return a + b;
+}
+
+// Reduce-scatter of 8 per-lane values over a warp: afterwards lane l holds the
+// warp sum of row ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
+__device__ __forceinline__ float butterfly8(float* v, int lane) {
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b4 ? v[i] : v[i + 4];
+    const float keep = b4 ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b3 ? v[i] : v[i + 2];
+    const float keep = b3 ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const float send = b2 ? v[0] : v[1];
+    const float keep = b2 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+__device__ __forceinline__ int butterfly_row(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+
+__device__ __forceinline__ float gelu_f(float x, int exact) {
+  if (exact) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+  const float k = 0.79788456080286536f;  // sqrt(2/pi)
+  return 0.5f * x * (1.0f + tanhf(k * (x + 0.044715f * x * x * x)));
+}
+
+__device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)u << 32) | (unsigned long long)(0xffffffffu - (uint32_t)idx);
+}
+
+// Consumer-wide sum (all ncw warps participate); `scratch` holds >= ncw floats.
+__device__ __forceinline__ float consumer_sum(float v, float* scratch, int ncw, int warp, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  consumer_sync(ncw * 32);
+  if (lane == 0) scratch[warp] = v;
+  consumer_sync(ncw * 32);
+  float t = 0.f;
+  for (int w = 0; w < ncw; ++w) t += scratch[w];
+  return t;
+}
+
+// ===========================================================================
+// Consumer
+// ===========================================================================
+template <int DPL>
+struct Consumer {
+  const Params& p;
+  const Smem& s;
+  const int tid, warp, lane, nct;
+  const uint32_t rank, cid;
+  const int pos, step, par;
+  const bool act;   // owns a live hidden chunk
+  uint32_t gs = 0;
+  int n_qkv = 0, n_att = 0, n_red = 0, n_rs = 0, n_events = 0;
+  // registers
+  float xn1[8], xn2[8], acc[8];
+  float gval = 0.f;                      // gelu(up) for row `lane` of the last UP stage
+  // attention state (valid lanes of a position group)
+  float qr[DPL], o[DPL], am, al;
+  // head argmax candidate (warp 0 lanes 0..7)
+  unsigned long long best = 0ull;
+
+  __device__ __forceinline__ Consumer(const Params& p_, const Smem& s_, int tid_, uint32_t rank_, uint32_t cid_,
+                      int pos_, int step_)
+      : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(p_.ncw * 32),
+        rank(rank_), cid(cid_), pos(pos_), step(step_), par(step_ & 1),
+        act(tid_ < (p_.h >> 3)) {}
+
+  __device__ __forceinline__ void release(int slot) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s.empty[slot]);
+  }
+
+  // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40)
+  __device__ __forceinline__ void layer_norm(const float* x, const float* g, const float* b, float* out) {
+    float sm = 0.f;
+    if (act)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sm += x[i];
+    const float mu = consumer_sum(sm, reinterpret_cast<float*>(s.misc) + 16, p.ncw, warp, lane) / p.h;
+    float sq = 0.f;
+    if (act)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sq += (x[i] - mu) * (x[i] - mu);
+    const float var = consumer_sum(sq, reinterpret_cast<float*>(s.misc) + 32, p.ncw, warp, lane) / p.h;
+    const float rstd = rsqrtf(var + p.eps);
+    if (act) {
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(g) + 2 * tid);
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(g) + 2 * tid + 1);
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(b) + 2 * tid);
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(b) + 2 * tid + 1);
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = (x[i] - mu) * rstd * gg[i] + bb[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = 0.f;
+    }
+  }
+
+  __device__ __forceinline__ void load_vec(const float* src, float* x) {
+    if (act) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(src) + 2 * tid);
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(src) + 2 * tid + 1);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    }
+  }
+
+  // Row-dot of the stage's rows with `xv`; returns the final row sums through
+  // wred (after a consumer barrier).  Returns the wred buffer used.
+  __device__ __forceinline__ float* rowdot_stage(const unsigned char* slot, int n, const float* xv) {
+    float v[kRows];
+    if (act) {
+      uint4 w[kRows];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+        if (r < n) w[r] = *reinterpret_cast<const uint4*>(slot + (size_t)r * p.h * 2 + tid * 16);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) v[r] = (r < n) ? dot8(w[r], xv) : 0.f;
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) v[r] = 0.f;
+    }
+    const float t = butterfly8(v, lane);
+    float* wr = s.wred + (n_rs & 1) * p.ncw * kRows;
+    ++n_rs;
+    if ((lane & 3) == 0) wr[warp * kRows + butterfly_row(lane)] = t;
+    return wr;
+  }
+
+  __device__ __forceinline__ float row_total(const float* wr, int r) {
+    float t = 0.f;
+    for (int w = 0; w < p.ncw; ++w) t += wr[w * kRows + r];
+    return t;
+  }
+
+  // acc += coef(r) * row r, for the stage's rows (transposed projections).
+  // (coef may shuffle, so every lane runs the loop; only owners accumulate.)
+  template <class F>
+  __device__ __forceinline__ void rowacc_stage(const unsigned char* slot, int n, F coef) {
+    for (int r = 0; r < n; ++r) {
+      const float c = coef(r);
+      if (act) {
+        const uint4 w = *reinterpret_cast<const uint4*>(slot + (size_t)r * p.h * 2 + tid * 16);
+        float f[8];
+        h8_to_f32(w, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(c, f[i], acc[i]);
+      }
+    }
+  }
+
+  // ---- attention -----------------------------------------------------------
+  __device__ __forceinline__ int tpp() const { return p.d / DPL; }
+
+  // Rotated component j of a head vector stored at `v` (RoPE pairs (i, i+rd/2),
+  // nf/golden.py:68-92); table row = this step's position.
+  __device__ __forceinline__ float rope_at(const float* v, int j) const {
+    const int half = p.rd >> 1;
+    if (j >= p.rd) return v[j];
+    const int i = j < half ? j : j - half;
+    const float2 cs = __ldg(&p.rope[(size_t)pos * half + i]);
+    return j < half ? v[j] * cs.x - v[j + half] * cs.y : v[j - half] * cs.y + v[j] * cs.x;
+  }
+
+  __device__ __forceinline__ void attention_begin() {
+    const int T = tpp();
+    const int sub = lane % T;
+    am = -INFINITY;
+    al = 0.f;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      o[i] = 0.f;
+      qr[i] = rope_at(s.ybuf, sub * DPL + i);
+    }
+  }
+
+  // Online-softmax update of this lane's group with score s2 (log2 domain)
+  // and value row `vr` (this lane's DPL dims).
+  __device__ __forceinline__ void att_update(float s2, const float* vv) {
+    const float mn = fmaxf(am, s2);
+    const float alpha = exp2f(am - mn);
+    const float w = exp2f(s2 - mn);
+    al = al * alpha + w;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) o[i] = fmaf(o[i], alpha, w * vv[i]);
+    am = mn;
+  }
+
+  __device__ __forceinline__ float group_dot(float part, int T, int sub) {
+    for (int off = 1; off < T; off <<= 1) {
+      const float t = __shfl_down_sync(0xffffffffu, part, off);
+      if (sub + off < T) part += t;
+    }
+    return __shfl_sync(0xffffffffu, part, lane - sub);
+  }
+
+  __device__ __forceinline__ void attention_stage(const unsigned char* slot, int n) {
+    const int T = tpp(), gpw = 32 / T;
+    const int sub = lane % T, gw = lane / T;
+    const bool valid = gw < gpw;
+    const int ng = p.ncw * gpw;
+    const __half* K = reinterpret_cast<const __half*>(slot);
+    const __half* Vv = K + (size_t)n * p.d;
+    for (int b = warp * gpw; b < n; b += ng) {
+      const int pp = b + gw;
+      const bool has = valid && pp < n;
+      float part = 0.f;
+      float vv[DPL];
+      if (has) {
+        const uint4* kr = reinterpret_cast<const uint4*>(K + (size_t)pp * p.d + sub * DPL);
+        const uint4* vr = reinterpret_cast<const uint4*>(Vv + (size_t)pp * p.d + sub * DPL);
+#pragma unroll
+        for (int c = 0; c < DPL / 8; ++c) {
+          float kf[8];
+          h8_to_f32(kr[c], kf);
+          h8_to_f32(vr[c], vv + 8 * c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) part = fmaf(qr[8 * c + i], kf[i], part);
+        }
+      }
+      const float sc = group_dot(part, T, sub);
+      if (has) att_update(sc * p.scale_log2, vv);
+    }
+  }
+
+  // The freshly appended token (position pos) on the last rank, from ybuf (fp32).
+  __device__ __forceinline__ void attention_new_token() {
+    if (warp != 0) return;
+    const int T = tpp();
+    const int sub = lane % T;
+    const bool has = lane < T;
+    float part = 0.f, vv[DPL];
+    if (has) {
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int j = sub * DPL + i;
+        part = fmaf(qr[i], rope_at(s.ybuf + p.d, j), part);
+        vv[i] = s.ybuf[2 * p.d + j];
+      }
+    }
+    const float sc = group_dot(part, T, sub);
+    if (has) att_update(sc * p.scale_log2, vv);
+  }
+
+  __device__ __forceinline__ void merge_into(float& m, float& l, float* oo, float m2, float l2,
+                                             const float* o2) {
+    if (!(l2 > 0.f)) return;
+    if (!(l > 0.f)) {
+      m = m2;
+      l = l2;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) oo[i] = o2[i];
+      return;
+    }
+    const float M = fmaxf(m, m2);
+    const float fa = exp2f(m - M), fb = exp2f(m2 - M);
+    l = l * fa + l2 * fb;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) oo[i] = oo[i] * fa + o2[i] * fb;
+    m = M;
+  }
+
+  // Groups -> warp -> CTA -> cluster (DSMEM) -> context vector in s.ctx.
+  __device__ __forceinline__ void attention_finish() {
+    const int T = tpp(), gpw = 32 / T, sub = lane % T;
+    const int d = p.d;
+    // 1) fold the warp's groups into group 0 (lanes 0..T-1)
+    for (int g2 = 1; g2 < gpw; ++g2) {
+      const int src = g2 * T + sub;
+      const float m2 = __shfl_sync(0xffffffffu, am, src);
+      const float l2 = __shfl_sync(0xffffffffu, al, src);
+      float o2[DPL];
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) o2[i] = __shfl_sync(0xffffffffu, o[i], src);
+      if (lane < T) merge_into(am, al, o, m2, l2, o2);
+    }
+    float* ws = s.wst + warp * s.wst_stride;
+    if (lane < T) {
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) ws[sub * DPL + i] = o[i];
+      if (lane == 0) {
+        ws[d] = am;
+        ws[d + 1] = al;
+      }
+    }
+    consumer_sync(nct);
+    // 2) CTA state, published to every rank's attst[rank]
+    float M = -INFINITY;
+    for (int w = 0; w < p.ncw; ++w) {
+      const float* wv = s.wst + w * s.wst_stride;
+      if (wv[d + 1] > 0.f) M = fmaxf(M, wv[d]);
+    }
+    float Lsum = 0.f;
+    for (int w = 0; w < p.ncw; ++w) {
+      const float* wv = s.wst + w * s.wst_stride;
+      if (wv[d + 1] > 0.f) Lsum += wv[d + 1] * exp2f(wv[d] - M);
+    }
+    const uint32_t my = smem_u32(s.attst + rank * s.attst_stride);
+    for (int t = tid; t < d + 2; t += nct) {
+      float val;
+      if (t < d) {
+        val = 0.f;
+        for (int w = 0; w < p.ncw; ++w) {
+          const float* wv = s.wst + w * s.wst_stride;
+          if (wv[d + 1] > 0.f) val += wv[t] * exp2f(wv[d] - M);
+        }
+      } else {
+        val = (t == d) ? M : Lsum;
+      }
+      for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(my + 4u * t, r), val);
+    }
+    consumer_sync(nct);
+    if (tid == 0)
+      for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_att, r);
+    mbar_wait_cluster(s.bar_att, n_att & 1, p.err, 12);
+    ++n_att;
+    // 3) merge the C rank states in rank order -> context
+    float Mc = -INFINITY;
+    for (int r = 0; r < p.C; ++r) {
+      const float* a = s.attst + r * s.attst_stride;
+      if (a[d + 1] > 0.f) Mc = fmaxf(Mc, a[d]);
+    }
+    float Lc = 0.f;
+    for (int r = 0; r < p.C; ++r) {
+      const float* a = s.attst + r * s.attst_stride;
+      if (a[d + 1] > 0.f) Lc += a[d + 1] * exp2f(a[d] - Mc);
+    }
+    for (int t = tid; t < d; t += nct) {
+      float val = 0.f;
+      for (int r = 0; r < p.C; ++r) {
+        const float* a = s.attst + r * s.attst_stride;
+        if (a[d + 1] > 0.f) val += a[t] * exp2f(a[d] - Mc);
+      }
+      s.ctx[t] = val / Lc;
+    }
+    consumer_sync(nct);
+  }
+
+  // ---- QKV exchange ----------------------------------------------------------
+  __device__ __forceinline__ void qkv_exchange_done(int head) {
+    consumer_sync(nct);  // all ybuf stores of this rank issued (warp 0 wrote them)
+    if (tid == 0)
+      for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_qkv, r);
+    mbar_wait_cluster(s.bar_qkv, n_qkv & 1, p.err, 11);
+    ++n_qkv;
+    // Rank 0 appends this step's rotated key and value to the cache (fp16).
+    if (rank == 0) {
+      const LayerW& W = p.layers[cur_layer];
+      const size_t off = ((size_t)head * p.max_seq + pos) * p.d;
+      for (int j = tid; j < p.d; j += nct) {
+        W.kc[off + j] = __float2half_rn(rope_at(s.ybuf + p.d, j));
+        W.vc[off + j] = __float2half_rn(s.ybuf[2 * p.d + j]);
+      }
+    }
+    attention_begin();
+  }
+
+  int cur_layer = 0;
+
+  // ---- layer-end reduction -------------------------------------------------
+  // event 0: parallel END, 1: sequential SYNC (attention half), 2: sequential END
+  __device__ __forceinline__ void reduce_event(int event, int lrel) {
+    const int h = p.h;
+    // 1) split-K partials of the cluster -> rank 0 via DSMEM
+    if (p.C > 1) {
+      if (rank != 0) {
+        if (act) {
+          const uint32_t dst = mapa(smem_u32(s.red_in + (size_t)(rank - 1) * h + tid * 8), 0);
+          st_cluster_v4(dst, acc[0], acc[1], acc[2], acc[3]);
+          st_cluster_v4(dst + 16, acc[4], acc[5], acc[6], acc[7]);
+        }
+        consumer_sync(nct);
+        if (tid == 0) mbar_arrive_cluster(s.bar_red, 0);
+      } else {
+        mbar_wait_cluster(s.bar_red, n_red & 1, p.err, 13);
+        if (act)
+          for (int r = 1; r < p.C; ++r) {
+            const float4 a = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8);
+            const float4 b = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8 + 4);
+            acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+            acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+          }
+      }
+      ++n_red;
+    }
+    if (rank == 0 && act) {
+      float4* dst = reinterpret_cast<float4*>(p.part + (size_t)cid * h + tid * 8);
+      __stcg(dst, make_float4(acc[0], acc[1], acc[2], acc[3]));
+      __stcg(dst + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+    }
+    // 2) grid barrier #1
+    consumer_sync(nct);
+    if (tid == 0) {
+      grid_sync(p.gbar, gridDim.x, p.err);
+      if (blockIdx.x == 0 && n_events == 0) {
+        // every CTA has read (pos, step) before arriving: advance them now
+        p.state[0] = pos + (p.advance_pos ? 1 : 0);
+        p.state[1] = step + 1;
+      }
+    }
+    ++n_events;
+    consumer_sync(nct);
+    // 3) fold: this CTA owns elements [e0, e0 + epc), partial sums over
+    //    clusters k = kg, kg + nkg, ... then a fixed-order combine.
+    const int G = gridDim.x;
+    const int epc = (h + G - 1) / G;
+    const int e0 = blockIdx.x * epc;
+    const int nkg = max(1, nct / max(epc, 1));
+    const LayerW& W = p.layers[cur_layer];
+    const float* xin = p.xs + (size_t)lrel * h;
+    auto finish = [&](int e, float t) {
+      if (event == 0) {
+        p.xs[(size_t)(lrel + 1) * h + e] = __ldcg(xin + e) + __ldg(W.bo + e) + __ldg(W.bd + e) + t;
+      } else if (event == 1) {
+        p.rbuf[e] = __ldcg(xin + e) + __ldg(W.bo + e) + t;
+      } else {
+        p.xs[(size_t)(lrel + 1) * h + e] = __ldcg(p.rbuf + e) + __ldg(W.bd + e) + t;
+      }
+    };
+    if (nkg == 1) {
+      // few CTAs: each thread folds whole elements
+      for (int ee = tid; ee < epc; ee += nct) {
+        const int e = e0 + ee;
+        if (e >= h) break;
+        float t = 0.f;
+        for (int k = 0; k < p.n_clusters; ++k) t += __ldcg(p.part + (size_t)k * h + e);
+        finish(e, t);
+      }
+    } else {
+      if (e0 < h) {
+        const int ee = tid % epc, kg = tid / epc;
+        if (kg < nkg) {
+          float t = 0.f;
+          const int e = e0 + ee;
+          if (e < h)
+            for (int k = kg; k < p.n_clusters; k += nkg) t += __ldcg(p.part + (size_t)k * h + e);
+          s.fold[kg * epc + ee] = t;
+        }
+      }
+      consumer_sync(nct);
+      if (e0 < h && tid < epc && e0 + tid < h) {
+        float t = 0.f;
+        for (int kg = 0; kg < nkg; ++kg) t += s.fold[kg * epc + tid];
+        finish(e0 + tid, t);
+      }
+    }
+    // 4) grid barrier #2
+    consumer_sync(nct);
+    if (tid == 0) grid_sync(p.gbar, gridDim.x, p.err);
+    consumer_sync(nct);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  }
+
+  // ---- main loop --------------------------------------------------------------
+  __device__ __forceinline__ void run() {
+    const int h = p.h;
+    for (int l = p.l0; l < p.l1; ++l) {
+      cur_layer = l;
+      const int lrel = l - p.l0;
+      const LayerW& W = p.layers[l];
+      float x[8];
+      if (l == p.l0 && p.in_mode == IN_TOKEN) {
+        const int tok = s.misc[2];
+        if (act) {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(p.head.embed + (size_t)tok * h) + tid);
+          h8_to_f32(w, x);
+          if (blockIdx.x == 0) {
+            float4* dst = reinterpret_cast<float4*>(p.xs) + 2 * tid;
+            dst[0] = make_float4(x[0], x[1], x[2], x[3]);
+            dst[1] = make_float4(x[4], x[5], x[6], x[7]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = 0.f;
+        }
+      } else {
+        load_vec(p.xs + (size_t)lrel * h, x);
+      }
+      layer_norm(x, W.ln1g, W.ln1b, xn1);
+      if (p.parallel) layer_norm(x, W.ln2g, W.ln2b, xn2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+
+      for (;;) {
+        const int slot = gs % p.n_slots;
+        mbar_wait(&s.full[slot], (gs / p.n_slots) & 1u, p.err, 20);
+        const Desc dsc = s.desc[slot];
+        const unsigned char* buf = s.ring + (size_t)slot * p.slot_bytes;
+        ++gs;
+        const int head = dsc.flags >> 8;
+        const bool last = dsc.flags & F_LAST;
+        if (dsc.type == ST_QKV) {
+          float* wr = rowdot_stage(buf, dsc.n, xn1);
+          release(slot);
+          consumer_sync(nct);
+          if (warp == 0 && lane < dsc.n) {
+            const int row = dsc.a + lane;  // row within the head's 3d rows
+            const float y = row_total(wr, lane) + __ldg(W.bqkv + head * 3 * p.d + row);
+            const uint32_t a = smem_u32(s.ybuf + row);
+            for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(a, r), y);
+          }
+          if (last) qkv_exchange_done(head);
+        } else if (dsc.type == ST_KV) {
+          attention_stage(buf, dsc.n);
+          release(slot);
+          if (last) {
+            if ((int)rank == p.C - 1) attention_new_token();
+            attention_finish();
+          }
+        } else if (dsc.type == ST_WO) {
+          const float* cx = s.ctx + dsc.a;
+          rowacc_stage(buf, dsc.n, [&](int r) { return cx[r]; });
+          release(slot);
+        } else if (dsc.type == ST_UP) {
+          float* wr = rowdot_stage(buf, dsc.n, xn2);
+          release(slot);
+          consumer_sync(nct);
+          if (lane < dsc.n) gval = gelu_f(row_total(wr, lane) + __ldg(W.bup + dsc.a + lane), p.gelu_exact);
+        } else if (dsc.type == ST_DOWN) {
+          const float g = gval;
+          rowacc_stage(buf, dsc.n, [&](int r) { return __shfl_sync(0xffffffffu, g, r); });
+          release(slot);
+        } else if (dsc.type == ST_SYNC) {
+          release(slot);
+          reduce_event(1, lrel);
+          float r[8];
+          load_vec(p.rbuf, r);
+          layer_norm(r, W.ln2g, W.ln2b, xn2);
+        } else if (dsc.type == ST_END) {
+          release(slot);
+          reduce_event(p.parallel ? 0 : 2, lrel);
+          break;
+        } else {
+          // unexpected stage type: poison and stop
+          fail_timeout(p.err, 99);
+        }
+      }
+    }
+    if (p.head_mode != HEAD_NONE) run_head();
+  }
+
+  __device__ __forceinline__ void run_head() {
+    const int h = p.h;
+    const int L = p.l1 - p.l0;
+    float x[8];
+    load_vec(p.xs + (size_t)L * h, x);
+    if (p.head_mode == HEAD_LM) {
+      layer_norm(x, p.head.lnfg, p.head.lnfb, xn1);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xn1[i] = x[i];
+    }
+    for (;;) {
+      const int slot = gs % p.n_slots;
+      mbar_wait(&s.full[slot], (gs / p.n_slots) & 1u, p.err, 21);
+      const Desc dsc = s.desc[slot];
+      const unsigned char* buf = s.ring + (size_t)slot * p.slot_bytes;
+      ++gs;
+      if (dsc.type == ST_LM) {
+        float* wr = rowdot_stage(buf, dsc.n, xn1);
+        release(slot);
+        consumer_sync(nct);
+        if (warp == 0 && lane < dsc.n) {
+          const int row = dsc.a + lane;
+          const float lg = row_total(wr, lane);
+          if (p.logits) p.logits[row] = lg;
+          const unsigned long long k = pack_argmax(lg, row);
+          best = k > best ? k : best;
+        }
+      } else {
+        release(slot);
+        if (warp == 0) {
+          unsigned long long b = best;
+#pragma unroll
+          for (int o2 = 16; o2 > 0; o2 >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o2);
+            b = t > b ? t : b;
+          }
+          if (lane == 0 && b) atomicMax(&p.amax[par], b);
+        }
+        break;
+      }
+    }
+  }
+};
+
+// ===========================================================================
+// Kernel
+// ===========================================================================
+template <int DPL, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Layout L = make_layout(p);
+  const Smem s = carve(smem_raw, L, p);
+  const int tid = threadIdx.x;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t cid = cluster_id_x();
+
+  if (tid == 0) {
+    for (int i = 0; i < p.n_slots; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], p.ncw);
+    }
+    mbar_init(s.bar_qkv, p.C);
+    mbar_init(s.bar_att, p.C);
+    mbar_init(s.bar_red, p.C > 1 ? p.C - 1 : 1);
+    fence_mbar_init();
+    const int pos = *reinterpret_cast<volatile int*>(p.state);
+    const int step = *reinterpret_cast<volatile int*>(p.state + 1);
+    s.misc[0] = pos;
+    s.misc[1] = step;
+    const int par = step & 1;
+    int tok = 0;
+    if (p.in_mode == IN_TOKEN) {
+      const unsigned long long prev = *reinterpret_cast<volatile unsigned long long*>(p.amax + (par ^ 1));
+      tok = (int)(0xffffffffu - (uint32_t)(prev & 0xffffffffull));
+      if (tok < 0 || tok >= p.V) tok = 0;
+    }
+    s.misc[2] = tok;
+    if (blockIdx.x == 0) {
+      // Slots of the other parity are idle during this launch: reset them.
+      for (int i = 0; i < p.ctr_stride; ++i) p.ctr[(par ^ 1) * p.ctr_stride + i] = 0;
+      if (p.head_mode != HEAD_NONE) p.amax[par] = 0ull;
+      if (p.in_mode == IN_TOKEN && step < p.max_seq) p.tokens[step] = tok;
+    }
+  }
+  cluster_sync_all();
+  const int pos = s.misc[0], step = s.misc[1];
+
+  const int warp = tid >> 5;
+  if (warp == p.ncw) {
+    if ((tid & 31) == 0) {
+      Producer prod(p, s);
+      prod.run(pos, step & 1, rank, cid);
+    }
+  } else if (warp < p.ncw) {
+    Consumer<DPL> c(p, s, tid, rank, cid, pos, step);
+    c.run();
+  }
+  cluster_sync_all();
+}
+
+// Explicit instantiations used by the host launcher: 8 head dims per lane,
+// block of <= 12 warps (hidden <= 2816) or <= 17 warps (hidden <= 4096).
+template __global__ void decode_kernel<8, 384>(const Params);
+template __global__ void decode_kernel<8, 544>(const Params);
+
+}  // namespace nfb
+
+// ===========================================================================
+// Host-side launch helpers (kept in this TU so the template stubs are local)
+// ===========================================================================
+namespace nfb {
+
+// `variant`: 0 -> block <= 384 threads, 1 -> block <= 544 threads.
+const void* decode_kernel_ptr(int variant) {
+  return variant == 0 ? reinterpret_cast<const void*>(&decode_kernel<8, 384>)
+                      : reinterpret_cast<const void*>(&decode_kernel<8, 544>);
+}
+
+cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
+                          bool cooperative) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (cooperative) {
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    na = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  if (dpl == 0) return cudaLaunchKernelEx(&cfg, decode_kernel<8, 384>, p);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<8, 544>, p);
+}
+
+cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, decode_kernel_ptr(dpl), &cfg);
+}
+
+}  // namespace nfb

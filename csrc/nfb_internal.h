@@ -1,0 +1,111 @@
+// Internal types shared by the decode kernel and the host-side context.
+// Not part of the C-ABI (see include/nfb200.h for that).
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace nfb {
+
+// Weight stages carry at most this many matrix rows.
+constexpr int kRows = 8;
+// Upper bound on consumer warps (hidden <= 16 * 256 = 4096).
+constexpr int kMaxConsumerWarps = 16;
+
+// Per-layer device pointers: the "layer descriptor table" built once per
+// context (graph mode re-uses it for every step).
+struct LayerW {
+  const __half* wqkv;   // [3h][h]  reference layout, rows of head j = [3dj, 3d(j+1))
+  const __half* woT;    // [h][h]   W_out^T: row k multiplies context element k
+  const __half* wup;    // [m][h]
+  const __half* wdT;    // [m][h]   W_down^T: row j multiplies gelu(up)_j
+  const float* bqkv;    // [3h]
+  const float* bo;      // [h]
+  const float* bup;     // [m]
+  const float* bd;      // [h]
+  const float* ln1g;
+  const float* ln1b;
+  const float* ln2g;
+  const float* ln2b;
+  __half* kc;           // [H][max_seq][d]  keys, post-RoPE
+  __half* vc;           // [H][max_seq][d]
+};
+
+struct HeadW {
+  const __half* embed;    // [V][h]
+  const float* lnfg;      // [h]
+  const float* lnfb;      // [h]
+  const __half* unembed;  // [V][h]
+};
+
+enum InMode : int { IN_X = 0, IN_TOKEN = 1 };
+enum HeadMode : int { HEAD_NONE = 0, HEAD_PROBE = 1, HEAD_LM = 2 };
+
+struct Params {
+  // shape
+  int h, H, d, m, rd, V, max_seq;
+  float eps;
+  float scale_log2;     // log2(e) / sqrt(d)
+  int parallel;         // GPT-NeoX parallel residual
+  int gelu_exact;
+  int l0, l1;           // layer range of this launch
+  // decomposition
+  int C;                // cluster size (CTAs per cluster)
+  int n_clusters;
+  int ncw;              // consumer warps
+  int rows_qkv;         // 3d / C  QKV rows per CTA per head
+  int rows_o;           // d / C   W_out^T rows per CTA per head
+  int stage_rows;       // matrix rows per weight stage (<= kRows)
+  int n_slots;
+  int slot_bytes;
+  int kv_pos;           // positions per KV stage
+  // modes
+  int in_mode;
+  int head_mode;
+  int advance_pos;      // graph/decode mode: pos += 1 after the step
+  int dyn_mlp;          // 1: MLP chunks grabbed dynamically (not bitwise reproducible)
+  // pointers
+  const LayerW* layers;
+  HeadW head;
+  const float2* rope;   // [max_seq][rd/2] (cos, sin), fp32 from f64 host values
+  float* xs;            // [(l1-l0)+1][h] hidden states (xs[0] = block input)
+  float* rbuf;          // [h] sequential-residual temp
+  float* part;          // [n_clusters][h] cluster partial sums
+  int* ctr;             // [2][ctr_stride] dynamic chunk counters by step parity
+  int ctr_stride;
+  unsigned* gbar;       // [2] grid barrier count / generation
+  int* state;           // [0] pos, [1] step
+  unsigned long long* amax;  // [2] packed (ordered logit, ~index) by step parity
+  int* tokens;          // [max_seq] token consumed at each step
+  float* logits;        // [V] or null
+  int* err;             // device error word
+};
+
+// Shared-memory carve-up, computed identically on host and device.
+struct Layout {
+  int ring, full, empty, desc, bars, ybuf, attst, ctx, wst, wred, red_in, fold, misc, total;
+};
+
+__host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline Layout make_layout(const Params& p) {
+  Layout L;
+  int o = 0;
+  L.ring = o;   o += p.n_slots * p.slot_bytes;
+  o = align_up(o, 16);
+  L.full = o;   o += 8 * p.n_slots;
+  L.empty = o;  o += 8 * p.n_slots;
+  L.desc = o;   o += 16 * p.n_slots;
+  L.bars = o;   o += 8 * 4;
+  L.ybuf = o;   o += 4 * align_up(3 * p.d, 4);
+  L.attst = o;  o += 4 * p.C * align_up(p.d + 2, 4);
+  L.ctx = o;    o += 4 * align_up(p.d, 4);
+  L.wst = o;    o += 4 * p.ncw * align_up(p.d + 2, 4);
+  L.wred = o;   o += 4 * 2 * p.ncw * kRows;
+  L.red_in = o; o += 4 * (p.C - 1) * p.h;
+  L.fold = o;   o += 4 * 32 * p.ncw;
+  L.misc = o;   o += 4 * 64;
+  L.total = align_up(o, 128);
+  return L;
+}
+
+}  // namespace nfb

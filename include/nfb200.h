@@ -1,0 +1,150 @@
+/*
+ * nfb200.h -- C-ABI of the B200-native fused GPT-NeoX decode block.
+ *
+ * The drop-in boundary for the reference package `neoxfuse`
+ * (/root/reference/pkg/src/neoxfuse, "nf/" below).  The reference has no FFI:
+ * its boundary is a Python function-level API.  Each entry point names the
+ * reference interface it replaces; the Python shim `paper_2604_23553_b200`
+ * binds these symbols with ctypes.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Every function
+ * returns NFB_OK (0) or a negative status; nfb_last_error() returns a
+ * thread-local message for the last failure.  Host arrays are row-major in the
+ * reference layout.  A context is bound to one device and one CUDA stream and
+ * is not thread-safe (one context per decode stream, nf SPEC.md:227).
+ */
+#ifndef NFB200_H
+#define NFB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NFB_OK 0
+#define NFB_EINVAL (-1)      /* bad argument (reference: ValueError)            */
+#define NFB_ECUDA (-2)       /* CUDA runtime failure                            */
+#define NFB_ESTATE (-3)      /* call out of order (weights / KV not loaded)     */
+#define NFB_EUNSUPPORTED (-4) /* shape the sm_100a kernel does not support       */
+#define NFB_EDEVICE (-5)     /* device-side watchdog fired (hang guard)         */
+
+/* Element types of host arrays handed to the library. */
+#define NFB_F64 0
+#define NFB_F32 1
+#define NFB_F16 2
+
+/* Head modes of nfb_forward. */
+#define NFB_HEAD_NONE 0
+#define NFB_HEAD_PROBE 1 /* logits = unembed @ h            (nf/fidelity.py:139) */
+#define NFB_HEAD_LM 2    /* logits = unembed @ LN_f(h)      (nf/perfmodel.py:96) */
+
+typedef struct nfb_ctx nfb_ctx;
+
+/* Replaces ModelConfig (nf/config.py:11-49); rotary_dims = floor(pct*d_head). */
+typedef struct {
+  int hidden, n_heads, d_head, n_layers, d_mlp, rotary_dims, vocab;
+  double ln_eps, theta_base;
+  int parallel_residual; /* nf/config.py:22, default 1 */
+  int gelu_exact;        /* 0: tanh (nf/golden.py:164, reference default), 1: erf */
+} nfb_model_desc;
+
+/* Replaces BlockWeights (nf/weights.py:24-37): reference shapes [out, in]. */
+typedef struct {
+  const void *ln1_gain, *ln1_bias, *qkv_weight, *qkv_bias, *out_weight, *out_bias;
+  const void *ln2_gain, *ln2_bias, *up_weight, *up_bias, *down_weight, *down_bias;
+} nfb_block_weights;
+
+typedef struct {
+  int grid;          /* CTAs (one per SM) */
+  int cluster_size;  /* CTAs per cluster (DSMEM group) */
+  int n_clusters;
+  int consumer_warps;
+  int stage_rows;
+  int n_slots;
+  int slot_bytes;
+  int kv_stage_pos;
+  int smem_bytes;
+  int max_seq;
+  int sm_count;
+} nfb_info;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int nfb_version(void);
+/* Thread-local text of the last error. */
+const char* nfb_last_error(void);
+
+/* Create a context for `desc` on `device` with KV capacity `max_seq` per layer.
+ * cluster_size 0 = default (2); max_clusters 0 = as many as fit co-resident.
+ * Replaces constructing ModelConfig + KVCache(n_heads, d_head) (nf/weights.py:135). */
+int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_size,
+               int max_clusters, nfb_ctx** out);
+int nfb_destroy(nfb_ctx* ctx);
+int nfb_get_info(nfb_ctx* ctx, nfb_info* info);
+
+/* Upload one layer's parameters (reference layout, dtype NFB_F64/F32/F16);
+ * rounded RNE to binary16 on upload.  Replaces passing `w` to
+ * fused_block_step / decoder_block_golden (nf/cluster.py:293, nf/golden.py:191). */
+int nfb_set_block_weights(nfb_ctx* ctx, int layer, const nfb_block_weights* w, int dtype);
+/* Device-side synth_weights(cfg, seed) (nf/weights.py:65-94), bit-exact, then RNE to fp16. */
+int nfb_synth_block_weights(nfb_ctx* ctx, int layer, uint64_t seed);
+/* Read back one layer's parameters as float32 in the reference layout
+ * (each pointer of `out` is a writable float* of the reference shape). */
+int nfb_read_block_weights(nfb_ctx* ctx, int layer, const nfb_block_weights* out);
+/* Embedding / final LN / unembedding ([vocab, hidden]); any pointer may be NULL
+ * to leave that tensor unset.  Replaces DecodeInstance.unembed (nf/fidelity.py:108). */
+int nfb_set_head(nfb_ctx* ctx, const void* embed, const void* lnf_gain, const void* lnf_bias,
+                 const void* unembed, int dtype);
+/* Device-side synthesis of the head with the documented recipe. */
+int nfb_synth_head(nfb_ctx* ctx, uint64_t seed);
+
+/* KV cache rows [n_heads][count][d_head] at positions [start, start+count).
+ * Replaces KVCache.from_arrays / keys() / values() (nf/weights.py:144-183). */
+int nfb_kv_write(nfb_ctx* ctx, int layer, int start, int count, const void* keys,
+                 const void* values, int dtype);
+int nfb_kv_read(nfb_ctx* ctx, int layer, int start, int count, float* keys, float* values);
+/* Synthetic pre-rotated prefix: 0.8660254 * uniform(-1,1) (variance 0.25) from
+ * the counter PRNG. */
+int nfb_kv_synth(nfb_ctx* ctx, int layer, int count, uint64_t seed);
+
+/* One decode step of one block at position `pos` (the cache must hold exactly
+ * `pos` positions; the new K/V is appended at `pos`).  x_in / x_out are HOST
+ * float32 [hidden].  Replaces fused_block_step (nf/cluster.py:291-369). */
+int nfb_block_step(nfb_ctx* ctx, int layer, int pos, const float* x_in, float* x_out);
+
+/* All layers (+ optional head) for one position, teacher-forced input vector.
+ * x_in HOST [hidden]; hidden_out HOST [(n_layers+1)][hidden] or NULL;
+ * logits_out HOST [vocab] or NULL.  Replaces one iteration of
+ * DecodeInstance.variant_logits (nf/fidelity.py:142-153). */
+int nfb_forward(nfb_ctx* ctx, int pos, const float* x_in, float* hidden_out, float* logits_out,
+                int head_mode);
+
+/* Greedy token decode with device-resident state (graph mode).
+ * nfb_begin_decode sets position and first input token; each nfb_decode_step
+ * embeds the previous argmax, runs all layers + LM head, argmax on device and
+ * advances the position.  `stream` may be NULL (context stream). */
+int nfb_begin_decode(nfb_ctx* ctx, int pos, int token);
+int nfb_decode_step(nfb_ctx* ctx, void* stream);
+/* End-to-end serving step with HOST buffers: copy `token` host->device,
+ * run one decode step (graph replay if captured, else a launch), copy the
+ * argmax device->host into *next_token and wait for it. */
+int nfb_step_token(nfb_ctx* ctx, int token, int* next_token);
+/* Capture one nfb_decode_step into a CUDA graph; replay it n times. */
+int nfb_graph_capture(nfb_ctx* ctx);
+int nfb_graph_replay(nfb_ctx* ctx, int n, void* stream);
+/* Tokens consumed by steps [0, n) and the argmax of the last step. */
+int nfb_read_tokens(nfb_ctx* ctx, int* tokens, int n, int* last_argmax);
+/* Hidden states [(n_layers+1)][hidden] and logits [vocab] of the last launch. */
+int nfb_read_hidden(nfb_ctx* ctx, float* out);
+int nfb_read_logits(nfb_ctx* ctx, float* out);
+/* Current device position / step counters. */
+int nfb_get_state(nfb_ctx* ctx, int* pos, int* step);
+/* Block until the context stream is idle; reports device-side failures. */
+int nfb_sync(nfb_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for event timing. */
+void* nfb_stream(nfb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NFB200_H */

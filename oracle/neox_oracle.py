@@ -389,3 +389,19 @@ class Model:
         xs = self.hidden_states(self.head["embed"][token])
         lg = self.logits(xs[-1])
         return greedy(lg), lg, xs
+
+
+# ---------------------------------------------------------------------------
+# Synthetic KV prefix recipe, as generated on the
+# device by nfb_kv_synth: 0.8660254037844386 * u (variance 0.25, the
+# reference's N(0,1)*0.5 scale -- nf/fidelity.py:168-169), rounded to fp16.
+
+def kv_seed(base: int, layer: int) -> int:
+    return (base + 0x10000 + layer) & _MASK64
+
+
+def synth_kv(s: Shape, count: int, seed: int):
+    n = s.n_heads * count * s.d_head
+    k = f16_round(0.8660254037844386 * uniform_stream(seed, 0, n)).reshape(s.n_heads, count, s.d_head)
+    v = f16_round(0.8660254037844386 * uniform_stream(seed, 1, n)).reshape(s.n_heads, count, s.d_head)
+    return k, v

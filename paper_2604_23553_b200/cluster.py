@@ -1,0 +1,245 @@
+"""``fused_block_step`` on B200 -- drop-in for ``neoxfuse.cluster`` (nf/cluster.py).
+
+The reference *simulates* a cluster of thread blocks in float64 numpy; here
+the same call runs the real sm_100a fused block kernel (``libnfb200.so``):
+one launch of clusters of ``C`` CTAs with DSMEM exchanges (QKV, softmax
+state merge, split-K partials) and a fixed-order cross-cluster fold.
+
+Numerics: fp16 weights and KV cache, fp32 activations / accumulation, fixed
+reduction order (deterministic run to run).  The reference's FP16-atomic
+*emulation* (``Precision.FP16``, nf/cluster.py:253-285) is not reproduced:
+the B200 kernel has no FP16 atomics anywhere, so ``accumulation_precision``
+only affects the returned trace, exactly as ``plan`` does.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import warnings
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from .engine import Engine
+from .plans import FusionPlan, Op, kernel_layer_bytes
+
+_ONCHIP_ELEM = 4
+DEFAULT_N_BLOCKS = 4
+
+
+class Precision(Enum):
+    EXACT = "exact"
+    FP16 = "fp16"
+
+
+class ReductionKind(Enum):
+    RING = "ring"
+    TREE = "tree"
+    PERMUTED_ATOMIC = "permuted-atomic"
+
+
+def ring_steps(n: int) -> int:
+    if n < 1:
+        raise ValueError("empty reduction")
+    return n - 1
+
+
+def tree_steps(n: int) -> int:
+    if n < 1:
+        raise ValueError("empty reduction")
+    return math.ceil(math.log2(n)) if n > 1 else 0
+
+
+@dataclass(frozen=True)
+class ReductionStrategy:
+    kind: ReductionKind
+    seed: int = 0
+
+    def steps(self, n: int) -> int:
+        return tree_steps(n) if self.kind is ReductionKind.TREE else ring_steps(n)
+
+
+RING = ReductionStrategy(ReductionKind.RING)
+TREE = ReductionStrategy(ReductionKind.TREE)
+
+
+@dataclass(frozen=True)
+class ClusterSpec:
+    n_blocks: int = DEFAULT_N_BLOCKS
+    reduction: ReductionStrategy = TREE
+    accumulation_precision: Precision = Precision.EXACT
+    atomic_seed: int = 0
+
+    def __post_init__(self):
+        if self.n_blocks < 1:
+            raise ValueError("n_blocks must be >= 1")
+
+
+@dataclass
+class KernelTraceRecord:
+    name: str
+    bytes_offchip: int
+    bytes_onchip: int = 0
+    sync_steps: int = 0
+    dsmem_exchanges: int = 0
+
+
+@dataclass
+class ExecTrace:
+    records: list = field(default_factory=list)
+    device: dict = field(default_factory=dict)  # real launch shape on the GPU
+
+    @property
+    def kernel_count(self) -> int:
+        return len(self.records)
+
+    @property
+    def bytes_offchip(self) -> int:
+        return sum(r.bytes_offchip for r in self.records)
+
+    @property
+    def bytes_onchip(self) -> int:
+        return sum(r.bytes_onchip for r in self.records)
+
+    @property
+    def sync_steps(self) -> int:
+        return sum(r.sync_steps for r in self.records)
+
+    @property
+    def dsmem_exchanges(self) -> int:
+        return sum(r.dsmem_exchanges for r in self.records)
+
+
+def trace_to_jsonl(trace: ExecTrace) -> str:
+    rows = [json.dumps({"name": r.name, "bytes_offchip": r.bytes_offchip,
+                        "bytes_onchip": r.bytes_onchip, "sync_steps": r.sync_steps},
+                       sort_keys=True) for r in trace.records]
+    return "".join(line + "\n" for line in rows)
+
+
+def partition_kv(seq_len: int, n_blocks: int) -> list:
+    """Balanced contiguous ranges; the first seq_len % n_blocks get one extra
+    (nf/cluster.py:134-150).  The device kernel splits each head's history
+    across the CTAs of its cluster with exactly this rule."""
+    if seq_len < 0:
+        raise ValueError("seq_len must be >= 0")
+    if n_blocks < 1:
+        raise ValueError("n_blocks must be >= 1")
+    q, r = divmod(seq_len, n_blocks)
+    bounds = [0]
+    for b in range(n_blocks):
+        bounds.append(bounds[-1] + q + (b < r))
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
+def _resolve_reduction(strategy: ReductionStrategy, n: int) -> ReductionStrategy:
+    if strategy.kind is ReductionKind.TREE and n & (n - 1):
+        warnings.warn(f"tree reduction needs a power-of-two cluster, got {n}; falling back to ring",
+                      RuntimeWarning, stacklevel=3)
+        return ReductionStrategy(ReductionKind.RING, strategy.seed)
+    return strategy
+
+
+def build_trace(cfg, spec: ClusterSpec, plan: FusionPlan, seq_len: int, elem_size: int,
+                strategy: ReductionStrategy) -> ExecTrace:
+    """Trace records with the reference's accounting (nf/cluster.py:354-369)."""
+    n = spec.n_blocks
+    levels = strategy.steps(n)
+    recs = []
+    for kernel, nbytes in zip(plan.kernels, kernel_layer_bytes(plan, cfg, seq_len, elem_size)):
+        rec = KernelTraceRecord(kernel.name, nbytes)
+        if Op.ATTEND in kernel.ops:
+            rec.bytes_onchip += (n - 1) * cfg.n_heads * (cfg.d_head + 2) * _ONCHIP_ELEM
+            rec.sync_steps += levels
+            rec.dsmem_exchanges += n - 1
+        if Op.OUT_PROJ in kernel.ops:
+            rec.bytes_onchip += (n - 1) * cfg.hidden * _ONCHIP_ELEM
+            rec.sync_steps += levels
+            rec.dsmem_exchanges += n - 1
+        recs.append(rec)
+    return ExecTrace(records=recs)
+
+
+# ---------------------------------------------------------------------------
+# Device mirrors: one single-layer Engine per (shape, gelu); the KV cache of
+# the last host cache object is kept resident and only re-uploaded when the
+# caller's cache changed behind our back.
+
+class _Slot:
+    def __init__(self, engine):
+        self.engine = engine
+        self.weights = None      # the BlockWeights object last uploaded
+        self.cache = None        # the host cache object mirrored on device
+        self.cache_sig = None
+
+
+_SLOTS: dict = {}
+
+
+def _cache_sig(cache):
+    return (id(cache), len(cache), getattr(cache, "version", None))
+
+
+def _slot(cfg, gelu: str, need: int) -> _Slot:
+    key = (cfg.hidden, cfg.n_heads, cfg.d_head, cfg.d_mlp, cfg.rotary_dims, cfg.ln_eps,
+           cfg.theta_base, bool(cfg.parallel_residual), gelu)
+    s = _SLOTS.get(key)
+    if s is None or s.engine.max_seq < need:
+        cap = 256
+        while cap < need:
+            cap *= 2
+        if s is not None:
+            s.engine.close()
+        s = _Slot(Engine(cfg.with_(n_layers=1, vocab=1), max_seq=cap, gelu=gelu))
+        _SLOTS[key] = s
+    return s
+
+
+def release_device_state() -> None:
+    """Free the cached device contexts used by ``fused_block_step``."""
+    for s in _SLOTS.values():
+        s.engine.close()
+    _SLOTS.clear()
+
+
+def fused_block_step(x, w, cache, pos: int, cfg, spec: ClusterSpec, plan: FusionPlan,
+                     gelu: str = "tanh", elem_size: int = 2):
+    """One decode step of the block on the GPU (nf/cluster.py:291-369).
+
+    Returns ``(output [hidden] float64, ExecTrace)`` and appends this step's
+    (rotated) key and value to ``cache`` -- same contract as the reference.
+    """
+    plan.validate()
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (cfg.hidden,):
+        raise ValueError(f"input must have shape ({cfg.hidden},)")
+    if len(cache) != pos:
+        raise ValueError(f"cache holds {len(cache)} positions, expected {pos}")
+    strategy = _resolve_reduction(spec.reduction, spec.n_blocks)
+    if gelu not in ("tanh", "exact"):
+        raise ValueError(f"unknown gelu variant {gelu!r} (use 'exact' or 'tanh')")
+    if not np.all(np.isfinite(x)):
+        raise ValueError("non-finite activation")
+
+    s = _slot(cfg, gelu, pos + 1)
+    eng = s.engine
+    if s.weights is not w:
+        eng.set_block_weights(0, w)
+        s.weights = w
+    if s.cache is not cache or s.cache_sig != _cache_sig(cache) or eng.kv_len(0) != pos:
+        keys = np.asarray(cache.keys())
+        values = np.asarray(cache.values())
+        eng.kv_write(0, 0, keys.reshape(cfg.n_heads, pos, cfg.d_head),
+                     values.reshape(cfg.n_heads, pos, cfg.d_head))
+    out = eng.block_step(0, pos, x).astype(np.float64)
+    k, v = eng.kv_read(0, pos, 1)
+    cache.append(k[:, 0, :].astype(np.float64), v[:, 0, :].astype(np.float64))
+    s.cache, s.cache_sig = cache, _cache_sig(cache)
+
+    trace = build_trace(cfg, spec, plan, len(cache), elem_size, strategy)
+    inf = eng.info
+    trace.device = {"grid": inf["grid"], "cluster_size": inf["cluster_size"],
+                    "n_clusters": inf["n_clusters"], "kernel": "nfb::decode_kernel"}
+    return out, trace

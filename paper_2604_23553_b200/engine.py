@@ -1,0 +1,247 @@
+"""``Engine``: one device context of the fused decode block (C-ABI wrapper).
+
+An Engine owns, on one GPU: fp16 weights of ``cfg.n_layers`` blocks, the KV
+cache ``[layer][head][max_seq][d_head]`` (fp16, keys post-RoPE), the optional
+embedding / final LN / unembedding, and the persistent launch state (graph,
+device-resident position and token).  All compute runs in the sm_100a kernel
+of ``libnfb200.so``; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, fptr
+from .weights import TENSOR_NAMES, BlockWeights
+
+HEAD_MODES = {None: _lib.HEAD_NONE, "none": _lib.HEAD_NONE, "probe": _lib.HEAD_PROBE, "lm": _lib.HEAD_LM}
+
+
+def _dtype_code(a: np.ndarray) -> int:
+    if a.dtype == np.float64:
+        return _lib.NFB_F64
+    if a.dtype == np.float32:
+        return _lib.NFB_F32
+    if a.dtype == np.float16:
+        return _lib.NFB_F16
+    raise TypeError(f"unsupported dtype {a.dtype}")
+
+
+def _host(a, dtype=None) -> np.ndarray:
+    a = np.asarray(a)
+    if dtype is not None:
+        a = a.astype(dtype, copy=False)
+    elif a.dtype not in (np.float64, np.float32, np.float16):
+        a = a.astype(np.float64)
+    return np.ascontiguousarray(a)
+
+
+class Engine:
+    def __init__(self, cfg, max_seq: int, gelu: str = "tanh", device: int = 0,
+                 cluster_size: int = 0, max_clusters: int = 0):
+        if gelu not in ("tanh", "exact"):
+            raise ValueError(f"unknown gelu variant {gelu!r} (use 'exact' or 'tanh')")
+        self.lib = _lib.load()
+        self.cfg, self.gelu, self.max_seq = cfg, gelu, int(max_seq)
+        desc = _lib.ModelDesc(cfg.hidden, cfg.n_heads, cfg.d_head, cfg.n_layers, cfg.d_mlp,
+                              cfg.rotary_dims, cfg.vocab, float(cfg.ln_eps), float(cfg.theta_base),
+                              1 if cfg.parallel_residual else 0, 1 if gelu == "exact" else 0)
+        h = C.c_void_p()
+        check(self.lib.nfb_create(C.byref(desc), device, self.max_seq, cluster_size, max_clusters,
+                                  C.byref(h)), "nfb_create")
+        self._h = h
+        self._kv_len = [0] * cfg.n_layers
+
+    # ---- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.nfb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def info(self) -> dict:
+        inf = _lib.Info()
+        check(self.lib.nfb_get_info(self._h, C.byref(inf)), "nfb_get_info")
+        return {n: getattr(inf, n) for n, _ in _lib.Info._fields_}
+
+    @property
+    def stream(self) -> int:
+        """cudaStream_t of the context (for torch.cuda.ExternalStream timing)."""
+        return self.lib.nfb_stream(self._h) or 0
+
+    # ---- parameters --------------------------------------------------------
+    def set_block_weights(self, layer: int, w) -> None:
+        if isinstance(w, dict):
+            w = BlockWeights(**w)
+        arrs = [_host(getattr(w, n)) for n in TENSOR_NAMES]
+        dt = {a.dtype for a in arrs}
+        if len(dt) != 1:
+            arrs = [a.astype(np.float64) for a in arrs]
+        ptrs = _lib.BlockWeightPtrs(*[a.ctypes.data for a in arrs])
+        check(self.lib.nfb_set_block_weights(self._h, layer, C.byref(ptrs), _dtype_code(arrs[0])),
+              "nfb_set_block_weights")
+
+    def synth_block_weights(self, layer: int, seed: int) -> None:
+        check(self.lib.nfb_synth_block_weights(self._h, layer, C.c_uint64(seed & (2**64 - 1))),
+              "nfb_synth_block_weights")
+
+    def read_block_weights(self, layer: int) -> BlockWeights:
+        """Device parameters (fp16 values) as float32 arrays in the reference layout."""
+        from .weights import tensor_shapes
+        arrs = {n: np.empty(shape, np.float32) for n, shape in tensor_shapes(self.cfg).items()}
+        ptrs = _lib.BlockWeightPtrs(*[arrs[n].ctypes.data for n in TENSOR_NAMES])
+        check(self.lib.nfb_read_block_weights(self._h, layer, C.byref(ptrs)), "nfb_read_block_weights")
+        return BlockWeights(**arrs)
+
+    def set_head(self, embed=None, lnf_gain=None, lnf_bias=None, unembed=None) -> None:
+        arrs = [None if a is None else _host(a, np.float64) for a in (embed, lnf_gain, lnf_bias, unembed)]
+        ptrs = [None if a is None else C.c_void_p(a.ctypes.data) for a in arrs]
+        check(self.lib.nfb_set_head(self._h, *ptrs, _lib.NFB_F64), "nfb_set_head")
+
+    def synth_head(self, seed: int) -> None:
+        check(self.lib.nfb_synth_head(self._h, C.c_uint64(seed & (2**64 - 1))), "nfb_synth_head")
+
+    def synth_model(self, base_seed: int = 0) -> None:
+        """All layers with seed base+l and the head with seed base+n_layers
+        (oracle.neox_oracle.layer_seed/head_seed)."""
+        for l in range(self.cfg.n_layers):
+            self.synth_block_weights(l, base_seed + l)
+        self.synth_head(base_seed + self.cfg.n_layers)
+
+    # ---- KV cache ----------------------------------------------------------
+    def kv_len(self, layer: int = 0) -> int:
+        return self._kv_len[layer]
+
+    def kv_write(self, layer: int, start: int, keys, values) -> None:
+        k, v = _host(keys), _host(values)
+        if k.shape != v.shape or k.ndim != 3:
+            raise ValueError("keys/values must share shape [n_heads, seq, d_head]")
+        if v.dtype != k.dtype:
+            v = v.astype(k.dtype)
+        check(self.lib.nfb_kv_write(self._h, layer, start, k.shape[1], C.c_void_p(k.ctypes.data),
+                                    C.c_void_p(v.ctypes.data), _dtype_code(k)), "nfb_kv_write")
+        self._kv_len[layer] = start + k.shape[1]
+
+    def kv_read(self, layer: int, start: int = 0, count: int | None = None):
+        count = self._kv_len[layer] - start if count is None else count
+        shape = (self.cfg.n_heads, count, self.cfg.d_head)
+        k = np.empty(shape, np.float32)
+        v = np.empty(shape, np.float32)
+        check(self.lib.nfb_kv_read(self._h, layer, start, count, fptr(k), fptr(v)), "nfb_kv_read")
+        return k, v
+
+    def kv_synth(self, layer: int, count: int, seed: int) -> None:
+        check(self.lib.nfb_kv_synth(self._h, layer, count, C.c_uint64(seed & (2**64 - 1))), "nfb_kv_synth")
+        self._kv_len[layer] = count
+
+    def kv_synth_all(self, count: int, base_seed: int) -> None:
+        """Synthetic prefix of every layer with seed kv_seed(base, l)."""
+        for l in range(self.cfg.n_layers):
+            self.kv_synth(l, count, kv_seed(base_seed, l))
+
+    # ---- compute -----------------------------------------------------------
+    def block_step(self, layer: int, pos: int, x) -> np.ndarray:
+        x32 = np.ascontiguousarray(x, dtype=np.float32)
+        if x32.shape != (self.cfg.hidden,):
+            raise ValueError(f"input must have shape ({self.cfg.hidden},)")
+        out = np.empty(self.cfg.hidden, np.float32)
+        check(self.lib.nfb_block_step(self._h, layer, pos, fptr(x32), fptr(out)), "nfb_block_step")
+        self._kv_len[layer] = pos + 1
+        return out
+
+    def forward(self, pos: int, x, head: str | None = None, hidden: bool = True):
+        """All layers at position ``pos`` for input vector ``x``; returns
+        (hidden states [(L+1), h] or None, logits [V] or None)."""
+        x32 = np.ascontiguousarray(x, dtype=np.float32)
+        if x32.shape != (self.cfg.hidden,):
+            raise ValueError(f"input must have shape ({self.cfg.hidden},)")
+        mode = HEAD_MODES[head]
+        hs = np.empty((self.cfg.n_layers + 1, self.cfg.hidden), np.float32) if hidden else None
+        lg = np.empty(self.cfg.vocab, np.float32) if mode else None
+        check(self.lib.nfb_forward(self._h, pos, fptr(x32), fptr(hs) if hs is not None else None,
+                                   fptr(lg) if lg is not None else None, mode), "nfb_forward")
+        self._kv_len = [pos + 1] * self.cfg.n_layers
+        return hs, lg
+
+    # ---- greedy decode with device-resident state ---------------------------
+    def begin_decode(self, pos: int, token: int) -> None:
+        check(self.lib.nfb_begin_decode(self._h, pos, token), "nfb_begin_decode")
+        self._decode_start = pos
+
+    def decode_step(self, stream: int = 0) -> None:
+        check(self.lib.nfb_decode_step(self._h, C.c_void_p(stream) if stream else None), "nfb_decode_step")
+        self._kv_len = [x + 1 for x in self._kv_len]
+
+    def step_token(self, token: int) -> int:
+        """Serving step with host buffers: token in (H2D), next greedy token out (D2H)."""
+        out = C.c_int()
+        check(self.lib.nfb_step_token(self._h, int(token), C.byref(out)), "nfb_step_token")
+        self._kv_len = [x + 1 for x in self._kv_len]
+        return out.value
+
+    def graph_capture(self) -> None:
+        check(self.lib.nfb_graph_capture(self._h), "nfb_graph_capture")
+
+    def graph_replay(self, n: int = 1, stream: int = 0) -> None:
+        check(self.lib.nfb_graph_replay(self._h, n, C.c_void_p(stream) if stream else None),
+              "nfb_graph_replay")
+        self._kv_len = [x + n for x in self._kv_len]
+
+    def read_tokens(self, n: int):
+        """(tokens consumed by steps 0..n-1, argmax of the latest step)."""
+        toks = np.zeros(n, np.int32)
+        last = C.c_int()
+        check(self.lib.nfb_read_tokens(self._h, toks.ctypes.data_as(C.POINTER(C.c_int)), n,
+                                       C.byref(last)), "nfb_read_tokens")
+        return toks, int(last.value)
+
+    def generate(self, token: int, pos: int, steps: int, graph: bool = True):
+        """Greedy decode ``steps`` tokens starting at ``pos`` with input ``token``.
+        Returns the generated token ids (argmax of each step)."""
+        self.begin_decode(pos, token)
+        if graph:
+            self.graph_capture()
+            self.graph_replay(steps)
+        else:
+            for _ in range(steps):
+                self.decode_step()
+        toks, last = self.read_tokens(steps)
+        return [int(t) for t in toks[1:]] + [last]
+
+    def read_hidden(self) -> np.ndarray:
+        out = np.empty((self.cfg.n_layers + 1, self.cfg.hidden), np.float32)
+        check(self.lib.nfb_read_hidden(self._h, fptr(out)), "nfb_read_hidden")
+        return out
+
+    def read_logits(self) -> np.ndarray:
+        out = np.empty(self.cfg.vocab, np.float32)
+        check(self.lib.nfb_read_logits(self._h, fptr(out)), "nfb_read_logits")
+        return out
+
+    def state(self):
+        pos, step = C.c_int(), C.c_int()
+        check(self.lib.nfb_get_state(self._h, C.byref(pos), C.byref(step)), "nfb_get_state")
+        return pos.value, step.value
+
+    def sync(self) -> None:
+        check(self.lib.nfb_sync(self._h), "nfb_sync")
+
+
+def kv_seed(base: int, layer: int) -> int:
+    """Seed of the synthetic KV prefix of one layer."""
+    return (base + 0x10000 + layer) & (2**64 - 1)
