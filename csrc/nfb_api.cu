@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -177,7 +178,7 @@ struct nfb_ctx {
   float2* rope = nullptr;
   float *xs = nullptr, *rbuf = nullptr, *part = nullptr, *logits = nullptr;
   int *ctr = nullptr, *state = nullptr, *tokens = nullptr, *err = nullptr;
-  unsigned* gbar = nullptr;
+  unsigned long long* gbar = nullptr;
   unsigned long long* amax = nullptr;
   int ctr_stride = 0;
   // pinned staging
@@ -187,6 +188,10 @@ struct nfb_ctx {
   cudaGraphExec_t gexec = nullptr;
   int decode_pos = -1;  // host mirror of the device position in decode mode
   int decode_step = 0;  // host mirror of the device step counter
+  unsigned long long* trace = nullptr;
+  int trace_stride = 0;
+  int dyn_mlp = 0;
+  int head_weight_pct = 130;
   unsigned long long* h_tok = nullptr;  // pinned [2]
   std::vector<void*> allocs;
 };
@@ -249,6 +254,10 @@ Params base_params(nfb_ctx* c) {
   p.tokens = c->tokens;
   p.logits = c->logits;
   p.err = c->err;
+  p.trace = c->trace;
+  p.trace_stride = c->trace_stride;
+  p.dyn_mlp = c->dyn_mlp;
+  p.head_weight_pct = c->head_weight_pct;
   return p;
 }
 
@@ -394,7 +403,10 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   e = max_active_clusters(c->dpl, C, c->block, c->smem, &nc);
   if (e != cudaSuccess || nc < 1)
     return bail(fail(NFB_ECUDA, std::string("no co-resident cluster fits: ") + cudaGetErrorString(e)));
+  if (max_clusters <= 0 && getenv("NFB_MAX_CLUSTERS")) max_clusters = atoi(getenv("NFB_MAX_CLUSTERS"));
   if (max_clusters > 0) nc = std::min(nc, max_clusters);
+  if (getenv("NFB_NO_COOP")) c->coop = false;
+  if (getenv("NFB_HEAD_WEIGHT")) c->head_weight_pct = atoi(getenv("NFB_HEAD_WEIGHT"));
   c->n_clusters = nc;
   c->grid = nc * C;
 
@@ -880,6 +892,37 @@ int nfb_step_token(nfb_ctx* c, int token, int* next_token) {
   c->decode_step += 1;
   for (auto& b : c->layers) b.kv_len = c->decode_pos;
   *next_token = (int)(0xffffffffu - (uint32_t)(c->h_tok[1] & 0xffffffffull));
+  return NFB_OK;
+}
+
+int nfb_set_option(nfb_ctx* c, int option, int value) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  cudaSetDevice(c->device);
+  if (option == NFB_OPT_TRACE) {
+    if (value && !c->trace) {
+      c->trace_stride = kTraceHeader + kTracePerLayer * c->desc.n_layers;
+      TRY(dalloc(c, &c->trace, (size_t)c->grid * c->trace_stride));
+    } else if (!value) {
+      c->trace = nullptr;  // buffer stays in allocs until destroy
+    }
+  } else if (option == NFB_OPT_DYNAMIC_MLP) {
+    c->dyn_mlp = value ? 1 : 0;
+  } else {
+    return fail(NFB_EINVAL, "unknown option");
+  }
+  if (c->gexec) {  // captured params are stale
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+  }
+  return NFB_OK;
+}
+
+int nfb_read_trace(nfb_ctx* c, unsigned long long* out, int n) {
+  if (!c || !out) return fail(NFB_EINVAL, "null argument");
+  if (!c->trace) return fail(NFB_ESTATE, "tracing not enabled");
+  TRY(nfb_sync(c));
+  const size_t total = (size_t)c->grid * c->trace_stride;
+  CK(cudaMemcpy(out, c->trace, std::min<size_t>(total, (size_t)n) * 8, cudaMemcpyDeviceToHost));
   return NFB_OK;
 }
 

@@ -38,13 +38,15 @@ enum StageType : int {
   ST_QKV = 1, ST_KV = 2, ST_WO = 3, ST_UP = 4, ST_DOWN = 5,
   ST_SYNC = 6, ST_END = 7, ST_LM = 8, ST_HEAD_END = 9
 };
-constexpr int F_LAST = 1;
+constexpr int F_LAST = 1;   // last stage of a head's QKV / KV / W_out group
+constexpr int F_FIRST = 2;  // first stage of a row-dot batch (QKV / UP / LM)
+constexpr int F_FLUSH = 4;  // row-dot batch complete: reduce across warps now
 
 struct Desc {
   int type;
   int a;      // first row / position
   int n;      // rows / positions in this stage
-  int flags;  // bit 0: last stage of its group; bits 8..: head index
+  int flags;  // F_* bits; bits 8..: head index (QKV/KV/WO) or row offset (DOWN)
 };
 
 struct Smem {
@@ -62,6 +64,7 @@ struct Smem {
   float* wred;
   float* red_in;
   float* fold;
+  float2* rope;   // (cos, sin) of this step's position, rd/2 entries
   int* misc;
   int attst_stride;
   int wst_stride;
@@ -83,6 +86,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, cons
   s.wred = reinterpret_cast<float*>(base + L.wred);
   s.red_in = reinterpret_cast<float*>(base + L.red_in);
   s.fold = reinterpret_cast<float*>(base + L.fold);
+  s.rope = reinterpret_cast<float2*>(base + L.rope);
   s.misc = reinterpret_cast<int*>(base + L.misc);
   s.attst_stride = align_up(p.d + 2, 4);
   s.wst_stride = align_up(p.d + 2, 4);
@@ -95,16 +99,24 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, cons
 struct Producer {
   const Params& p;
   const Smem& s;
-  uint32_t gs = 0;
+  int pslot = 0;
+  uint32_t pphase = 0;
   uint64_t pol;
+  unsigned long long wait_ns = 0;
 
   __device__ __forceinline__ Producer(const Params& p_, const Smem& s_) : p(p_), s(s_) { pol = policy_evict_first(); }
 
   __device__ __forceinline__ void push(int type, int a, int n, int flags, const void* src0, uint32_t b0,
                        const void* src1 = nullptr, uint32_t b1 = 0) {
-    const int slot = gs % p.n_slots;
-    const uint32_t ph = ((gs / p.n_slots) & 1u) ^ 1u;
-    mbar_wait(&s.empty[slot], ph, p.err, 10);
+    const int slot = pslot;
+    const uint32_t ph = pphase ^ 1u;
+    if (p.trace) {
+      const unsigned long long t0 = globaltimer();
+      mbar_wait(&s.empty[slot], ph, p.err, 10);
+      wait_ns += globaltimer() - t0;
+    } else {
+      mbar_wait(&s.empty[slot], ph, p.err, 10);
+    }
     s.desc[slot] = Desc{type, a, n, flags};
     const uint32_t bytes = b0 + b1;
     unsigned char* dst = s.ring + (size_t)slot * p.slot_bytes;
@@ -115,7 +127,10 @@ struct Producer {
     } else {
       mbar_arrive(&s.full[slot]);
     }
-    ++gs;
+    if (++pslot == p.n_slots) {
+      pslot = 0;
+      pphase ^= 1u;
+    }
   }
 
   int mlp_c0 = 0, mlp_c1 = 0;
@@ -125,7 +140,8 @@ struct Producer {
     if (k >= p.H) return 0;
     const int nh = (p.H - k + p.n_clusters - 1) / p.n_clusters;
     const int cnt = pos / p.C + (r < pos % p.C ? 1 : 0);
-    return (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
+    const long long b = (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
+    return b * p.head_weight_pct / 100;
   }
 
   // Static, byte-balanced MLP chunk ranges: every CTA evaluates the same
@@ -170,7 +186,8 @@ struct Producer {
         for (int r = 0; r < p.rows_qkv; r += p.stage_rows) {
           const int n = min(p.stage_rows, p.rows_qkv - r);
           const int last = (r + n >= p.rows_qkv) ? F_LAST : 0;
-          push(ST_QKV, q0 + r, n, tag | last, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h, n * rowb);
+          const int first = r == 0 ? F_FIRST : 0;
+          push(ST_QKV, q0 + r, n, tag | last | first, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h, n * rowb);
         }
         // KV history share (partition_kv: first hist % C ranks get one extra).
         const int base = pos / C, extra = pos % C;
@@ -193,35 +210,52 @@ struct Producer {
         }
       }
       if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
-      if (p.dyn_mlp) {
-        int* ctr = p.ctr + par * p.ctr_stride + lrel;
-        for (;;) {
-          const int r = atomicAdd(ctr, 1) * p.stage_rows;
-          if (r >= p.m) break;
-          const int n = min(p.stage_rows, p.m - r);
-          push(ST_UP, r, n, 0, W.wup + (size_t)r * h, n * rowb);
-          push(ST_DOWN, r, n, 0, W.wdT + (size_t)r * h, n * rowb);
+      // MLP chunks in pairs: UP(c), UP(c+1) [flush], DOWN(c), DOWN(c+1), so
+      // consumers do one cross-warp reduction per 2 chunks.
+      int* ctr = p.ctr + par * p.ctr_stride + lrel;
+      int next = mlp_c0;
+      for (;;) {
+        int ca, cb;
+        if (p.dyn_mlp) {
+          ca = atomicAdd(ctr, 1);
+          if (ca * p.stage_rows >= p.m) break;
+          cb = atomicAdd(ctr, 1);
+          if (cb * p.stage_rows >= p.m) cb = -1;
+        } else {
+          if (next >= mlp_c1) break;
+          ca = next;
+          cb = next + 1 < mlp_c1 ? next + 1 : -1;
+          next += 2;
         }
-      } else {
-        for (int c = mlp_c0; c < mlp_c1; ++c) {
-          const int r = c * p.stage_rows;
-          const int n = min(p.stage_rows, p.m - r);
-          push(ST_UP, r, n, 0, W.wup + (size_t)r * h, n * rowb);
-          push(ST_DOWN, r, n, 0, W.wdT + (size_t)r * h, n * rowb);
+        const int ra = ca * p.stage_rows, na = min(p.stage_rows, p.m - ra);
+        push(ST_UP, ra, na, F_FIRST | (cb < 0 ? F_FLUSH : 0), W.wup + (size_t)ra * h, na * rowb);
+        int rb = 0, nb = 0;
+        if (cb >= 0) {
+          rb = cb * p.stage_rows;
+          nb = min(p.stage_rows, p.m - rb);
+          push(ST_UP, rb, nb, F_FLUSH, W.wup + (size_t)rb * h, nb * rowb);
         }
+        push(ST_DOWN, ra, na, 0, W.wdT + (size_t)ra * h, na * rowb);
+        if (cb >= 0) push(ST_DOWN, rb, nb, na << 8, W.wdT + (size_t)rb * h, nb * rowb);
       }
       push(ST_END, 0, 0, 0, nullptr, 0);
     }
     if (p.head_mode != HEAD_NONE) {
       int* ctr = p.ctr + par * p.ctr_stride + (p.l1 - p.l0);
       for (;;) {
-        const int r = atomicAdd(ctr, 1) * p.stage_rows;
-        if (r >= p.V) break;
-        const int n = min(p.stage_rows, p.V - r);
-        push(ST_LM, r, n, 0, p.head.unembed + (size_t)r * h, n * rowb);
+        const int ra = atomicAdd(ctr, 1) * p.stage_rows;
+        if (ra >= p.V) break;
+        int rb = atomicAdd(ctr, 1) * p.stage_rows;
+        if (rb >= p.V) rb = -1;
+        const int na = min(p.stage_rows, p.V - ra);
+        push(ST_LM, ra, na, F_FIRST | (rb < 0 ? F_FLUSH : 0), p.head.unembed + (size_t)ra * h, na * rowb);
+        if (rb < 0) break;
+        const int nb = min(p.stage_rows, p.V - rb);
+        push(ST_LM, rb, nb, F_FLUSH, p.head.unembed + (size_t)rb * h, nb * rowb);
       }
       push(ST_HEAD_END, 0, 0, 0, nullptr, 0);
     }
+    if (p.trace) p.trace[(size_t)blockIdx.x * p.trace_stride + 0] = wait_ns;
   }
 };
 
@@ -236,6 +270,32 @@ __device__ __forceinline__ void h8_to_f32(const uint4& w, float* f) {
     f[2 * i] = t.x;
     f[2 * i + 1] = t.y;
   }
+}
+
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) {
+  return (unsigned long long)__float_as_uint(v.x) | ((unsigned long long)__float_as_uint(v.y) << 32);
+}
+
+__device__ __forceinline__ float2 bits_f2(unsigned long long b) {
+  return make_float2(__uint_as_float((unsigned)b), __uint_as_float((unsigned)(b >> 32)));
+}
+
+// Packed fp32x2 FMA (sm_100 FFMA2): a * b + c element-wise.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return bits_f2(d);
+}
+
+// 8 fp16 weights . 8 fp32 inputs with packed FMAs (two interleaved chains).
+__device__ __forceinline__ float dot8x2(const uint4& w, const float2* x) {
+  const __half2* hp = reinterpret_cast<const __half2*>(&w);
+  float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+  a = ffma2(__half22float2(hp[0]), x[0], a);
+  b = ffma2(__half22float2(hp[1]), x[1], b);
+  a = ffma2(__half22float2(hp[2]), x[2], a);
+  b = ffma2(__half22float2(hp[3]), x[3], b);
+  return (a.x + b.x) + (a.y + b.y);
 }
 
 __device__ __forceinline__ float dot8(const uint4& w, const float* x) {
@@ -282,6 +342,13 @@ __device__ __forceinline__ int butterfly_row(int lane) {
   return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
 }
 
+// 2^x with the MUFU (ex2.approx, ~2 ulp); -inf -> 0.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float gelu_f(float x, int exact) {
   if (exact) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
   const float k = 0.79788456080286536f;  // sqrt(2/pi)
@@ -317,8 +384,18 @@ struct Consumer {
   const uint32_t rank, cid;
   const int pos, step, par;
   const bool act;   // owns a live hidden chunk
-  uint32_t gs = 0;
-  int n_qkv = 0, n_att = 0, n_red = 0, n_rs = 0, n_events = 0;
+  const int col;    // 16-byte column this thread reads from a weight row (0 if !act)
+  const int rowb;   // bytes per weight row (hidden * 2)
+  bool kv_first = false;
+  int pend = 0;        // rows accumulated in the current row-dot batch
+  int gbuf = 0;        // wred double-buffer of MLP / LM batches
+  float qbias = 0.f;   // this thread's QKV bias (row tid of this rank's QKV rows)
+  float gbias = 0.f;   // up bias of batch row `lane`
+  int lm_a0 = 0, lm_n0 = 0, lm_a1 = 0;
+  unsigned long long kv_ns = 0, kvwait_ns = 0;
+  int slot = 0;     // ring position of the next stage
+  uint32_t phase = 0;
+  int n_qkv = 0, n_att = 0, n_red = 0, n_events = 0;
   // registers
   float xn1[8], xn2[8], acc[8];
   float gval = 0.f;                      // gelu(up) for row `lane` of the last UP stage
@@ -331,11 +408,37 @@ struct Consumer {
                       int pos_, int step_)
       : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(p_.ncw * 32),
         rank(rank_), cid(cid_), pos(pos_), step(step_), par(step_ & 1),
-        act(tid_ < (p_.h >> 3)) {}
+        act(tid_ < (p_.h >> 3)), col(tid_ < (p_.h >> 3) ? tid_ : 0), rowb(p_.h * 2) {}
 
-  __device__ __forceinline__ void release(int slot) {
+  __device__ __forceinline__ void advance() {
+    if (++slot == p.n_slots) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+
+  unsigned long long wait_ns = 0;
+
+  __device__ __forceinline__ void stamp(int idx) {
+    if (p.trace && tid == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + idx] = globaltimer();
+  }
+  __device__ __forceinline__ void stamp_layer(int lrel, int k) { stamp(kTraceHeader + kTracePerLayer * lrel + k); }
+
+  unsigned long long last_wait = 0;
+  __device__ __forceinline__ void wait_full(int sl, int code) {
+    if (p.trace && tid == 0) {
+      const unsigned long long t0 = globaltimer();
+      mbar_wait(&s.full[sl], phase, p.err, code);
+      last_wait = globaltimer() - t0;
+      wait_ns += last_wait;
+    } else {
+      mbar_wait(&s.full[sl], phase, p.err, code);
+    }
+  }
+
+  __device__ __forceinline__ void release(int sl) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&s.empty[slot]);
+    if (lane == 0) mbar_arrive(&s.empty[sl]);
   }
 
   // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40)
@@ -378,47 +481,62 @@ struct Consumer {
     }
   }
 
-  // Row-dot of the stage's rows with `xv`; returns the final row sums through
-  // wred (after a consumer barrier).  Returns the wred buffer used.
-  __device__ __forceinline__ float* rowdot_stage(const unsigned char* slot, int n, const float* xv) {
+  // All kRows rows of this thread's 16-byte column, issued back to back
+  // (rows >= n read as zero; inactive threads read column 0 and are masked by
+  // zero inputs / never store their accumulators).
+  __device__ __forceinline__ void load_rows(const unsigned char* sl, int n, uint4 (&w)[kRows]) const {
+    const unsigned char* b = sl + col * 16;
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+      w[r] = (r < n) ? *reinterpret_cast<const uint4*>(b + r * rowb) : make_uint4(0u, 0u, 0u, 0u);
+  }
+
+  // Row-dot of the stage's rows with `xv`: the warp sum of row r lands in
+  // wbase[r * ncw + warp] (combine across warps with row_total after a
+  // consumer barrier).
+  __device__ __forceinline__ void rowdot_stage(const unsigned char* sl, int n, const float* xv, float* wbase) {
+    uint4 w[kRows];
+    load_rows(sl, n, w);
+    float2 x2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x2[i] = make_float2(xv[2 * i], xv[2 * i + 1]);
     float v[kRows];
-    if (act) {
-      uint4 w[kRows];
 #pragma unroll
-      for (int r = 0; r < kRows; ++r)
-        if (r < n) w[r] = *reinterpret_cast<const uint4*>(slot + (size_t)r * p.h * 2 + tid * 16);
-#pragma unroll
-      for (int r = 0; r < kRows; ++r) v[r] = (r < n) ? dot8(w[r], xv) : 0.f;
-    } else {
-#pragma unroll
-      for (int r = 0; r < kRows; ++r) v[r] = 0.f;
-    }
+    for (int r = 0; r < kRows; ++r) v[r] = dot8x2(w[r], x2);
     const float t = butterfly8(v, lane);
-    float* wr = s.wred + (n_rs & 1) * p.ncw * kRows;
-    ++n_rs;
-    if ((lane & 3) == 0) wr[warp * kRows + butterfly_row(lane)] = t;
-    return wr;
+    const int row = butterfly_row(lane);
+    if ((lane & 3) == 0 && row < n) wbase[row * p.ncw + warp] = t;
   }
 
-  __device__ __forceinline__ float row_total(const float* wr, int r) {
-    float t = 0.f;
-    for (int w = 0; w < p.ncw; ++w) t += wr[w * kRows + r];
-    return t;
-  }
-
-  // acc += coef(r) * row r, for the stage's rows (transposed projections).
-  // (coef may shuffle, so every lane runs the loop; only owners accumulate.)
-  template <class F>
-  __device__ __forceinline__ void rowacc_stage(const unsigned char* slot, int n, F coef) {
-    for (int r = 0; r < n; ++r) {
-      const float c = coef(r);
-      if (act) {
-        const uint4 w = *reinterpret_cast<const uint4*>(slot + (size_t)r * p.h * 2 + tid * 16);
-        float f[8];
-        h8_to_f32(w, f);
+  __device__ __forceinline__ float row_total(const float* wrow) const {
+    float t[kMaxConsumerWarps];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(c, f[i], acc[i]);
-      }
+    for (int w = 0; w < kMaxConsumerWarps; ++w) t[w] = w < p.ncw ? wrow[w] : 0.f;
+    float a = 0.f;
+#pragma unroll
+    for (int w = 0; w < kMaxConsumerWarps; ++w) a += t[w];
+    return a;
+  }
+
+  // acc += coef[r] * row r over the stage's rows (transposed projections);
+  // coef[r] must be 0 for r >= n.
+  __device__ __forceinline__ void rowacc_stage(const unsigned char* sl, int n, const float (&coef)[kRows]) {
+    uint4 w[kRows];
+    load_rows(sl, n, w);
+    float2 a2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a2[i] = make_float2(acc[2 * i], acc[2 * i + 1]);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const __half2* hp = reinterpret_cast<const __half2*>(&w[r]);
+      const float2 c2 = make_float2(coef[r], coef[r]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a2[i] = ffma2(c2, __half22float2(hp[i]), a2[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] = a2[i].x;
+      acc[2 * i + 1] = a2[i].y;
     }
   }
 
@@ -431,7 +549,7 @@ struct Consumer {
     const int half = p.rd >> 1;
     if (j >= p.rd) return v[j];
     const int i = j < half ? j : j - half;
-    const float2 cs = __ldg(&p.rope[(size_t)pos * half + i]);
+    const float2 cs = s.rope[i];
     return j < half ? v[j] * cs.x - v[j + half] * cs.y : v[j - half] * cs.y + v[j] * cs.x;
   }
 
@@ -451,14 +569,16 @@ struct Consumer {
   // and value row `vr` (this lane's DPL dims).
   __device__ __forceinline__ void att_update(float s2, const float* vv) {
     const float mn = fmaxf(am, s2);
-    const float alpha = exp2f(am - mn);
-    const float w = exp2f(s2 - mn);
+    const float alpha = fast_exp2(am - mn);
+    const float w = fast_exp2(s2 - mn);
     al = al * alpha + w;
 #pragma unroll
     for (int i = 0; i < DPL; ++i) o[i] = fmaf(o[i], alpha, w * vv[i]);
     am = mn;
   }
 
+  // Segmented sum over the T lanes of each position group (T need not be a
+  // power of two: d_head = 80 gives T = 10), broadcast to the group.
   __device__ __forceinline__ float group_dot(float part, int T, int sub) {
     for (int off = 1; off < T; off <<= 1) {
       const float t = __shfl_down_sync(0xffffffffu, part, off);
@@ -467,32 +587,78 @@ struct Consumer {
     return __shfl_sync(0xffffffffu, part, lane - sub);
   }
 
-  __device__ __forceinline__ void attention_stage(const unsigned char* slot, int n) {
+  // One KV stage: each position group takes kPos consecutive positions per
+  // iteration; the T-lane segmented sums of all kPos scores are interleaved
+  // level by level (ILP kPos on the shuffle chain), then one online-softmax
+  // update folds the kPos positions in.
+  __device__ __forceinline__ void attention_stage(const unsigned char* sl, int n) {
+    constexpr int kPos = 8;
     const int T = tpp(), gpw = 32 / T;
     const int sub = lane % T, gw = lane / T;
     const bool valid = gw < gpw;
-    const int ng = p.ncw * gpw;
-    const __half* K = reinterpret_cast<const __half*>(slot);
+    const int span = p.ncw * gpw * kPos;
+    const __half* K = reinterpret_cast<const __half*>(sl);
     const __half* Vv = K + (size_t)n * p.d;
-    for (int b = warp * gpw; b < n; b += ng) {
-      const int pp = b + gw;
-      const bool has = valid && pp < n;
-      float part = 0.f;
-      float vv[DPL];
-      if (has) {
-        const uint4* kr = reinterpret_cast<const uint4*>(K + (size_t)pp * p.d + sub * DPL);
-        const uint4* vr = reinterpret_cast<const uint4*>(Vv + (size_t)pp * p.d + sub * DPL);
+    for (int b = warp * gpw * kPos; b < n; b += span) {
+      const int p0 = b + gw * kPos;
+      float sc[kPos];
+      uint4 vw[kPos][DPL / 8];
+#pragma unroll
+      for (int k = 0; k < kPos; ++k) {
+        const int ps = (valid && p0 + k < n) ? p0 + k : 0;
+        float part = 0.f;
 #pragma unroll
         for (int c = 0; c < DPL / 8; ++c) {
+          const uint4 kw = *reinterpret_cast<const uint4*>(K + (size_t)ps * p.d + sub * DPL + 8 * c);
+          vw[k][c] = *reinterpret_cast<const uint4*>(Vv + (size_t)ps * p.d + sub * DPL + 8 * c);
           float kf[8];
-          h8_to_f32(kr[c], kf);
-          h8_to_f32(vr[c], vv + 8 * c);
+          h8_to_f32(kw, kf);
 #pragma unroll
           for (int i = 0; i < 8; ++i) part = fmaf(qr[8 * c + i], kf[i], part);
         }
+        sc[k] = part;
       }
-      const float sc = group_dot(part, T, sub);
-      if (has) att_update(sc * p.scale_log2, vv);
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) {
+        const bool take = sub + off < T;
+#pragma unroll
+        for (int k = 0; k < kPos; ++k) {
+          const float t = __shfl_down_sync(0xffffffffu, sc[k], off);
+          sc[k] = take ? sc[k] + t : sc[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPos; ++k) sc[k] = __shfl_sync(0xffffffffu, sc[k], lane - sub) * p.scale_log2;
+      if (valid && p0 < n) {
+        float mn = am;
+#pragma unroll
+        for (int k = 0; k < kPos; ++k)
+          if (p0 + k < n) mn = fmaxf(mn, sc[k]);
+        const float alpha = fast_exp2(am - mn);  // am = -inf on the first fold -> 0
+        float w[kPos], wsum = 0.f;
+#pragma unroll
+        for (int k = 0; k < kPos; ++k) {
+          w[k] = (p0 + k < n) ? fast_exp2(sc[k] - mn) : 0.f;
+          wsum += w[k];
+        }
+        al = al * alpha + wsum;
+#pragma unroll
+        for (int c = 0; c < DPL / 8; ++c) {
+          float t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = o[8 * c + i] * alpha;
+#pragma unroll
+          for (int k = 0; k < kPos; ++k) {
+            float vf[8];
+            h8_to_f32(vw[k][c], vf);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = fmaf(w[k], vf[i], t[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[8 * c + i] = t[i];
+        }
+        am = mn;
+      }
     }
   }
 
@@ -526,7 +692,7 @@ struct Consumer {
       return;
     }
     const float M = fmaxf(m, m2);
-    const float fa = exp2f(m - M), fb = exp2f(m2 - M);
+    const float fa = fast_exp2(m - M), fb = fast_exp2(m2 - M);
     l = l * fa + l2 * fb;
 #pragma unroll
     for (int i = 0; i < DPL; ++i) oo[i] = oo[i] * fa + o2[i] * fb;
@@ -566,7 +732,7 @@ struct Consumer {
     float Lsum = 0.f;
     for (int w = 0; w < p.ncw; ++w) {
       const float* wv = s.wst + w * s.wst_stride;
-      if (wv[d + 1] > 0.f) Lsum += wv[d + 1] * exp2f(wv[d] - M);
+      if (wv[d + 1] > 0.f) Lsum += wv[d + 1] * fast_exp2(wv[d] - M);
     }
     const uint32_t my = smem_u32(s.attst + rank * s.attst_stride);
     for (int t = tid; t < d + 2; t += nct) {
@@ -575,7 +741,7 @@ struct Consumer {
         val = 0.f;
         for (int w = 0; w < p.ncw; ++w) {
           const float* wv = s.wst + w * s.wst_stride;
-          if (wv[d + 1] > 0.f) val += wv[t] * exp2f(wv[d] - M);
+          if (wv[d + 1] > 0.f) val += wv[t] * fast_exp2(wv[d] - M);
         }
       } else {
         val = (t == d) ? M : Lsum;
@@ -583,6 +749,7 @@ struct Consumer {
       for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(my + 4u * t, r), val);
     }
     consumer_sync(nct);
+    stamp_layer(cur_layer - p.l0, 7);
     if (tid == 0)
       for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_att, r);
     mbar_wait_cluster(s.bar_att, n_att & 1, p.err, 12);
@@ -596,17 +763,18 @@ struct Consumer {
     float Lc = 0.f;
     for (int r = 0; r < p.C; ++r) {
       const float* a = s.attst + r * s.attst_stride;
-      if (a[d + 1] > 0.f) Lc += a[d + 1] * exp2f(a[d] - Mc);
+      if (a[d + 1] > 0.f) Lc += a[d + 1] * fast_exp2(a[d] - Mc);
     }
     for (int t = tid; t < d; t += nct) {
       float val = 0.f;
       for (int r = 0; r < p.C; ++r) {
         const float* a = s.attst + r * s.attst_stride;
-        if (a[d + 1] > 0.f) val += a[t] * exp2f(a[d] - Mc);
+        if (a[d + 1] > 0.f) val += a[t] * fast_exp2(a[d] - Mc);
       }
       s.ctx[t] = val / Lc;
     }
     consumer_sync(nct);
+    stamp_layer(cur_layer - p.l0, 2);
   }
 
   // ---- QKV exchange ----------------------------------------------------------
@@ -616,6 +784,7 @@ struct Consumer {
       for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_qkv, r);
     mbar_wait_cluster(s.bar_qkv, n_qkv & 1, p.err, 11);
     ++n_qkv;
+    stamp_layer(cur_layer - p.l0, 1);
     // Rank 0 appends this step's rotated key and value to the cache (fp16).
     if (rank == 0) {
       const LayerW& W = p.layers[cur_layer];
@@ -661,8 +830,24 @@ struct Consumer {
       __stcg(dst, make_float4(acc[0], acc[1], acc[2], acc[3]));
       __stcg(dst + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
     }
+    // the fold's non-partial terms (x, biases) do not depend on the barrier:
+    // fetch them now so their latency hides under it
+    const int G = gridDim.x;
+    const int epc = (h + G - 1) / G;
+    const int e0 = blockIdx.x * epc;
+    const int nkg = max(1, nct / max(epc, 1));
+    const LayerW& W = p.layers[cur_layer];
+    const float* xin = p.xs + (size_t)lrel * h;
+    auto base_of = [&](int e) {
+      if (event == 0) return __ldcg(xin + e) + __ldg(W.bo + e) + __ldg(W.bd + e);
+      if (event == 1) return __ldcg(xin + e) + __ldg(W.bo + e);
+      return __ldcg(p.rbuf + e) + __ldg(W.bd + e);
+    };
+    float base = 0.f;
+    if (nkg > 1 && tid < epc && e0 + tid < h) base = base_of(e0 + tid);
     // 2) grid barrier #1
     consumer_sync(nct);
+    stamp_layer(lrel, 8);
     if (tid == 0) {
       grid_sync(p.gbar, gridDim.x, p.err);
       if (blockIdx.x == 0 && n_events == 0) {
@@ -673,22 +858,12 @@ struct Consumer {
     }
     ++n_events;
     consumer_sync(nct);
+    stamp_layer(lrel, 4);
     // 3) fold: this CTA owns elements [e0, e0 + epc), partial sums over
     //    clusters k = kg, kg + nkg, ... then a fixed-order combine.
-    const int G = gridDim.x;
-    const int epc = (h + G - 1) / G;
-    const int e0 = blockIdx.x * epc;
-    const int nkg = max(1, nct / max(epc, 1));
-    const LayerW& W = p.layers[cur_layer];
-    const float* xin = p.xs + (size_t)lrel * h;
-    auto finish = [&](int e, float t) {
-      if (event == 0) {
-        p.xs[(size_t)(lrel + 1) * h + e] = __ldcg(xin + e) + __ldg(W.bo + e) + __ldg(W.bd + e) + t;
-      } else if (event == 1) {
-        p.rbuf[e] = __ldcg(xin + e) + __ldg(W.bo + e) + t;
-      } else {
-        p.xs[(size_t)(lrel + 1) * h + e] = __ldcg(p.rbuf + e) + __ldg(W.bd + e) + t;
-      }
+    auto finish = [&](int e, float v) {
+      if (event == 1) p.rbuf[e] = v;
+      else p.xs[(size_t)(lrel + 1) * h + e] = v;
     };
     if (nkg == 1) {
       // few CTAs: each thread folds whole elements
@@ -696,8 +871,16 @@ struct Consumer {
         const int e = e0 + ee;
         if (e >= h) break;
         float t = 0.f;
-        for (int k = 0; k < p.n_clusters; ++k) t += __ldcg(p.part + (size_t)k * h + e);
-        finish(e, t);
+        int k = 0;
+        for (; k + 8 <= p.n_clusters; k += 8) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(p.part + (size_t)(k + u) * h + e);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) t += v[u];
+        }
+        for (; k < p.n_clusters; ++k) t += __ldcg(p.part + (size_t)k * h + e);
+        finish(e, base_of(e) + t);
       }
     } else {
       if (e0 < h) {
@@ -705,8 +888,17 @@ struct Consumer {
         if (kg < nkg) {
           float t = 0.f;
           const int e = e0 + ee;
-          if (e < h)
-            for (int k = kg; k < p.n_clusters; k += nkg) t += __ldcg(p.part + (size_t)k * h + e);
+          if (e < h) {
+            int k = kg;
+            for (; k + 3 * nkg < p.n_clusters; k += 4 * nkg) {
+              float v[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[u] = __ldcg(p.part + (size_t)(k + u * nkg) * h + e);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) t += v[u];
+            }
+            for (; k < p.n_clusters; k += nkg) t += __ldcg(p.part + (size_t)k * h + e);
+          }
           s.fold[kg * epc + ee] = t;
         }
       }
@@ -714,13 +906,15 @@ struct Consumer {
       if (e0 < h && tid < epc && e0 + tid < h) {
         float t = 0.f;
         for (int kg = 0; kg < nkg; ++kg) t += s.fold[kg * epc + tid];
-        finish(e0 + tid, t);
+        finish(e0 + tid, base + t);
       }
     }
     // 4) grid barrier #2
     consumer_sync(nct);
+    stamp_layer(lrel, 9);
     if (tid == 0) grid_sync(p.gbar, gridDim.x, p.err);
     consumer_sync(nct);
+    stamp_layer(lrel, 5);
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
   }
@@ -728,6 +922,7 @@ struct Consumer {
   // ---- main loop --------------------------------------------------------------
   __device__ __forceinline__ void run() {
     const int h = p.h;
+    stamp(2);
     for (int l = p.l0; l < p.l1; ++l) {
       cur_layer = l;
       const int lrel = l - p.l0;
@@ -752,56 +947,93 @@ struct Consumer {
       }
       layer_norm(x, W.ln1g, W.ln1b, xn1);
       if (p.parallel) layer_norm(x, W.ln2g, W.ln2b, xn2);
+      stamp_layer(lrel, 0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 
       for (;;) {
-        const int slot = gs % p.n_slots;
-        mbar_wait(&s.full[slot], (gs / p.n_slots) & 1u, p.err, 20);
-        const Desc dsc = s.desc[slot];
-        const unsigned char* buf = s.ring + (size_t)slot * p.slot_bytes;
-        ++gs;
+        const int sl = slot;
+        wait_full(sl, 20);
+        const Desc dsc = s.desc[sl];
+        const unsigned char* buf = s.ring + (size_t)sl * p.slot_bytes;
+        advance();
         const int head = dsc.flags >> 8;
         const bool last = dsc.flags & F_LAST;
         if (dsc.type == ST_QKV) {
-          float* wr = rowdot_stage(buf, dsc.n, xn1);
-          release(slot);
-          consumer_sync(nct);
-          if (warp == 0 && lane < dsc.n) {
-            const int row = dsc.a + lane;  // row within the head's 3d rows
-            const float y = row_total(wr, lane) + __ldg(W.bqkv + head * 3 * p.d + row);
-            const uint32_t a = smem_u32(s.ybuf + row);
-            for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(a, r), y);
+          kv_first = true;
+          if (dsc.flags & F_FIRST) {
+            pend = 0;
+            qbias = tid < p.rows_qkv ? __ldg(W.bqkv + head * 3 * p.d + (int)rank * p.rows_qkv + tid) : 0.f;
           }
-          if (last) qkv_exchange_done(head);
+          rowdot_stage(buf, dsc.n, xn1, s.wred + pend * p.ncw);
+          release(sl);
+          pend += dsc.n;
+          if (last) {
+            // all of this rank's QKV rows: one cross-warp combine, then
+            // publish y into every cluster rank's ybuf through DSMEM
+            consumer_sync(nct);
+            const int q0 = (int)rank * p.rows_qkv;
+            for (int t = tid; t < p.rows_qkv; t += nct) {
+              const float b = t < nct ? qbias : __ldg(W.bqkv + head * 3 * p.d + q0 + t);
+              const float y = row_total(s.wred + t * p.ncw) + b;
+              const uint32_t a = smem_u32(s.ybuf + q0 + t);
+              for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(a, r), y);
+            }
+            qkv_exchange_done(head);
+          }
         } else if (dsc.type == ST_KV) {
+          const unsigned long long ta = (p.trace && tid == 0) ? globaltimer() : 0ull;
           attention_stage(buf, dsc.n);
-          release(slot);
+          release(sl);
+          if (p.trace && tid == 0) {
+            kv_ns += globaltimer() - ta;
+            kvwait_ns += last_wait;
+          }
+          if (kv_first) {
+            stamp_layer(lrel, 6);
+            kv_first = false;
+          }
           if (last) {
             if ((int)rank == p.C - 1) attention_new_token();
             attention_finish();
           }
         } else if (dsc.type == ST_WO) {
-          const float* cx = s.ctx + dsc.a;
-          rowacc_stage(buf, dsc.n, [&](int r) { return cx[r]; });
-          release(slot);
+          float c[kRows];
+#pragma unroll
+          for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? s.ctx[dsc.a + r] : 0.f;
+          rowacc_stage(buf, dsc.n, c);
+          release(sl);
         } else if (dsc.type == ST_UP) {
-          float* wr = rowdot_stage(buf, dsc.n, xn2);
-          release(slot);
-          consumer_sync(nct);
-          if (lane < dsc.n) gval = gelu_f(row_total(wr, lane) + __ldg(W.bup + dsc.a + lane), p.gelu_exact);
+          if (dsc.flags & F_FIRST) pend = 0;
+          if (lane >= pend && lane < pend + dsc.n) gbias = __ldg(W.bup + dsc.a + lane - pend);
+          float* wb = s.wred + (gbuf * 2 * kRows + pend) * p.ncw;
+          rowdot_stage(buf, dsc.n, xn2, wb);
+          release(sl);
+          pend += dsc.n;
+          if (dsc.flags & F_FLUSH) {
+            consumer_sync(nct);
+            const float* wr = s.wred + (gbuf * 2 * kRows + lane) * p.ncw;
+            gval = lane < pend ? gelu_f(row_total(wr) + gbias, p.gelu_exact) : 0.f;
+            gbuf ^= 1;
+          }
         } else if (dsc.type == ST_DOWN) {
-          const float g = gval;
-          rowacc_stage(buf, dsc.n, [&](int r) { return __shfl_sync(0xffffffffu, g, r); });
-          release(slot);
+          const int off = dsc.flags >> 8;
+          float c[kRows];
+#pragma unroll
+          for (int r = 0; r < kRows; ++r) c[r] = __shfl_sync(0xffffffffu, gval, (off + r) & 31);
+#pragma unroll
+          for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? c[r] : 0.f;
+          rowacc_stage(buf, dsc.n, c);
+          release(sl);
         } else if (dsc.type == ST_SYNC) {
-          release(slot);
+          release(sl);
           reduce_event(1, lrel);
           float r[8];
           load_vec(p.rbuf, r);
           layer_norm(r, W.ln2g, W.ln2b, xn2);
         } else if (dsc.type == ST_END) {
-          release(slot);
+          release(sl);
+          stamp_layer(lrel, 3);
           reduce_event(p.parallel ? 0 : 2, lrel);
           break;
         } else {
@@ -811,10 +1043,17 @@ struct Consumer {
       }
     }
     if (p.head_mode != HEAD_NONE) run_head();
+    stamp(3);
+    if (p.trace && tid == 0) {
+      p.trace[(size_t)blockIdx.x * p.trace_stride + 1] = wait_ns;
+      p.trace[(size_t)blockIdx.x * p.trace_stride + 6] = kv_ns;
+      p.trace[(size_t)blockIdx.x * p.trace_stride + 7] = kvwait_ns;
+    }
   }
 
   __device__ __forceinline__ void run_head() {
     const int h = p.h;
+    stamp(4);
     const int L = p.l1 - p.l0;
     float x[8];
     load_vec(p.xs + (size_t)L * h, x);
@@ -825,24 +1064,35 @@ struct Consumer {
       for (int i = 0; i < 8; ++i) xn1[i] = x[i];
     }
     for (;;) {
-      const int slot = gs % p.n_slots;
-      mbar_wait(&s.full[slot], (gs / p.n_slots) & 1u, p.err, 21);
-      const Desc dsc = s.desc[slot];
-      const unsigned char* buf = s.ring + (size_t)slot * p.slot_bytes;
-      ++gs;
+      const int sl = slot;
+      wait_full(sl, 21);
+      const Desc dsc = s.desc[sl];
+      const unsigned char* buf = s.ring + (size_t)sl * p.slot_bytes;
+      advance();
       if (dsc.type == ST_LM) {
-        float* wr = rowdot_stage(buf, dsc.n, xn1);
-        release(slot);
-        consumer_sync(nct);
-        if (warp == 0 && lane < dsc.n) {
-          const int row = dsc.a + lane;
-          const float lg = row_total(wr, lane);
-          if (p.logits) p.logits[row] = lg;
-          const unsigned long long k = pack_argmax(lg, row);
-          best = k > best ? k : best;
+        if (dsc.flags & F_FIRST) {
+          pend = 0;
+          lm_a0 = dsc.a;
+          lm_n0 = dsc.n;
+        } else {
+          lm_a1 = dsc.a;
+        }
+        rowdot_stage(buf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * p.ncw);
+        release(sl);
+        pend += dsc.n;
+        if (dsc.flags & F_FLUSH) {
+          consumer_sync(nct);
+          if (warp == 0 && lane < pend) {
+            const int row = lane < lm_n0 ? lm_a0 + lane : lm_a1 + lane - lm_n0;
+            const float lg = row_total(s.wred + (gbuf * 2 * kRows + lane) * p.ncw);
+            if (p.logits) p.logits[row] = lg;
+            const unsigned long long k = pack_argmax(lg, row);
+            best = k > best ? k : best;
+          }
+          gbuf ^= 1;
         }
       } else {
-        release(slot);
+        release(sl);
         if (warp == 0) {
           unsigned long long b = best;
 #pragma unroll
@@ -852,6 +1102,7 @@ struct Consumer {
           }
           if (lane == 0 && b) atomicMax(&p.amax[par], b);
         }
+        stamp(5);
         break;
       }
     }
@@ -897,6 +1148,11 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
       if (p.head_mode != HEAD_NONE) p.amax[par] = 0ull;
       if (p.in_mode == IN_TOKEN && step < p.max_seq) p.tokens[step] = tok;
     }
+  }
+  __syncthreads();
+  {
+    const int half = p.rd >> 1;
+    for (int i = tid; i < half; i += blockDim.x) s.rope[i] = __ldg(&p.rope[(size_t)s.misc[0] * half + i]);
   }
   cluster_sync_all();
   const int pos = s.misc[0], step = s.misc[1];

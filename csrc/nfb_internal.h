@@ -63,6 +63,7 @@ struct Params {
   int head_mode;
   int advance_pos;      // graph/decode mode: pos += 1 after the step
   int dyn_mlp;          // 1: MLP chunks grabbed dynamically (not bitwise reproducible)
+  int head_weight_pct;  // static schedule: head-stage bytes weighted by this / 100
   // pointers
   const LayerW* layers;
   HeadW head;
@@ -72,17 +73,28 @@ struct Params {
   float* part;          // [n_clusters][h] cluster partial sums
   int* ctr;             // [2][ctr_stride] dynamic chunk counters by step parity
   int ctr_stride;
-  unsigned* gbar;       // [2] grid barrier count / generation
+  unsigned long long* gbar;  // grid barrier arrival counter (monotonic)
   int* state;           // [0] pos, [1] step
   unsigned long long* amax;  // [2] packed (ordered logit, ~index) by step parity
   int* tokens;          // [max_seq] token consumed at each step
   float* logits;        // [V] or null
   int* err;             // device error word
+  unsigned long long* trace;  // optional [grid][trace_stride] globaltimer stamps
+  int trace_stride;
 };
+
+// Trace slots (per CTA): 0 producer ring-full wait ns, 1 consumer data wait ns
+// (thread 0), 2 kernel start, 3 consumer end, 4 head start, 5 head end,
+// then per layer l at 8 + 8*l: 0 layer start, 1 QKV exchanged, 2 context
+// ready, 3 END reached, 4 after grid barrier #1, 5 after grid barrier #2,
+// 6 first KV stage done, 7 attention state published, 8 partial stored
+// (before barrier #1), 9 fold done (before barrier #2).
+constexpr int kTraceHeader = 8;
+constexpr int kTracePerLayer = 12;
 
 // Shared-memory carve-up, computed identically on host and device.
 struct Layout {
-  int ring, full, empty, desc, bars, ybuf, attst, ctx, wst, wred, red_in, fold, misc, total;
+  int ring, full, empty, desc, bars, ybuf, attst, ctx, wst, wred, red_in, fold, rope, misc, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -100,9 +112,10 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.attst = o;  o += 4 * p.C * align_up(p.d + 2, 4);
   L.ctx = o;    o += 4 * align_up(p.d, 4);
   L.wst = o;    o += 4 * p.ncw * align_up(p.d + 2, 4);
-  L.wred = o;   o += 4 * 2 * p.ncw * kRows;
+  L.wred = o;   o += 4 * p.ncw * (align_up(p.rows_qkv, 8) > 4 * kRows ? align_up(p.rows_qkv, 8) : 4 * kRows);
   L.red_in = o; o += 4 * (p.C - 1) * p.h;
   L.fold = o;   o += 4 * 32 * p.ncw;
+  L.rope = o;   o += 4 * align_up(p.rd, 4);
   L.misc = o;   o += 4 * 64;
   L.total = align_up(o, 128);
   return L;

@@ -149,24 +149,32 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// Sense-free generation barrier over all CTAs of the grid (all co-resident:
-// one CTA per SM, launch checked against cudaOccupancyMaxActiveClusters).
+// Grid barrier over all CTAs of the grid (all co-resident: one CTA per SM,
+// launch checked against cudaOccupancyMaxActiveClusters).  The 64-bit arrival
+// counter only ever grows: every barrier instance adds exactly nblocks, so the
+// instance an arrival belongs to ends at the next multiple of nblocks above the
+// value it observed.  One acq_rel RMW per CTA, acquire polling, no SC fences.
 // Called by ONE thread per CTA after a CTA-level barrier.
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, int* err) {
-  const unsigned gen = ld_acquire_u32(bar + 1);
-  __threadfence();
-  const unsigned arrived = atomicAdd(bar, 1u);
-  if (arrived == nblocks - 1) {
-    atomicExch(bar, 0u);
-    __threadfence();
-    atomicAdd(bar + 1, 1u);
-  } else {
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_u32(bar + 1) == gen) {
-      if (globaltimer() - t0 > kTimeoutNs) fail_timeout(err, 3);
-    }
+__device__ __forceinline__ unsigned long long atom_add_acqrel_u64(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned nblocks, int* err) {
+  const unsigned long long old = atom_add_acqrel_u64(bar, 1ull);
+  const unsigned long long target = (old / nblocks + 1ull) * nblocks;
+  if (old + 1ull == target) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_u64(bar) < target) {
+    if (globaltimer() - t0 > kTimeoutNs) fail_timeout(err, 3);
   }
-  __threadfence();
 }
 
 }  // namespace nfb

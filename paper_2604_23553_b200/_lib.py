@@ -16,6 +16,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "nfb200.h")
 NFB_OK, NFB_EINVAL, NFB_ECUDA, NFB_ESTATE, NFB_EUNSUPPORTED, NFB_EDEVICE = 0, -1, -2, -3, -4, -5
 NFB_F64, NFB_F32, NFB_F16 = 0, 1, 2
 HEAD_NONE, HEAD_PROBE, HEAD_LM = 0, 1, 2
+OPT_TRACE, OPT_DYNAMIC_MLP = 1, 2
 
 
 class ModelDesc(C.Structure):
@@ -75,6 +76,8 @@ SIGNATURES = {
     "nfb_read_logits": (_I, [_P, _FP]),
     "nfb_get_state": (_I, [_P, _IP, _IP]),
     "nfb_sync": (_I, [_P]),
+    "nfb_set_option": (_I, [_P, _I, _I]),
+    "nfb_read_trace": (_I, [_P, C.POINTER(C.c_ulonglong), _I]),
     "nfb_stream": (_P, [_P]),
 }
 

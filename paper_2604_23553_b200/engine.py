@@ -238,6 +238,19 @@ class Engine:
         check(self.lib.nfb_get_state(self._h, C.byref(pos), C.byref(step)), "nfb_get_state")
         return pos.value, step.value
 
+    def set_option(self, option: str, value: bool) -> None:
+        code = {"trace": _lib.OPT_TRACE, "dynamic_mlp": _lib.OPT_DYNAMIC_MLP}[option]
+        check(self.lib.nfb_set_option(self._h, code, int(bool(value))), "nfb_set_option")
+
+    def read_trace(self) -> np.ndarray:
+        """Per-CTA phase stamps of the last launch: [grid, 8 + 12*n_layers] (ns)."""
+        inf = self.info
+        stride = 8 + 12 * self.cfg.n_layers
+        out = np.zeros((inf["grid"], stride), np.uint64)
+        check(self.lib.nfb_read_trace(self._h, out.ctypes.data_as(C.POINTER(C.c_ulonglong)), out.size),
+              "nfb_read_trace")
+        return out
+
     def sync(self) -> None:
         check(self.lib.nfb_sync(self._h), "nfb_sync")
 
