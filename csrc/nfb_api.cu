@@ -192,6 +192,8 @@ struct nfb_ctx {
   int trace_stride = 0;
   int dyn_mlp = 0;
   int head_weight_pct = 130;
+  int debug = 0;
+  int pf_ahead = 0;  // L2 prefetcher lead (bytes); measured: no gain at C2
   unsigned long long* h_tok = nullptr;  // pinned [2]
   std::vector<void*> allocs;
 };
@@ -258,6 +260,8 @@ Params base_params(nfb_ctx* c) {
   p.trace_stride = c->trace_stride;
   p.dyn_mlp = c->dyn_mlp;
   p.head_weight_pct = c->head_weight_pct;
+  p.pf_ahead = c->pf_ahead;
+  p.debug = c->debug;
   return p;
 }
 
@@ -383,7 +387,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
 
   c->ncw = (m.hidden / 8 + 31) / 32;
-  c->block = (c->ncw + 1) * 32;
+  c->block = (c->ncw + 2) * 32;  // consumers + ring producer warp + L2 prefetcher warp
   c->dpl = c->block <= 384 ? 0 : 1;  // kernel variant (max threads per block)
   c->stage_rows = m.hidden >= 4096 ? 4 : kRows;
   c->slot_bytes = std::max(c->stage_rows * m.hidden * 2, 4 * m.d_head * 2 * 2);
@@ -407,6 +411,8 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (max_clusters > 0) nc = std::min(nc, max_clusters);
   if (getenv("NFB_NO_COOP")) c->coop = false;
   if (getenv("NFB_HEAD_WEIGHT")) c->head_weight_pct = atoi(getenv("NFB_HEAD_WEIGHT"));
+  if (getenv("NFB_DEBUG")) c->debug = atoi(getenv("NFB_DEBUG"));
+  if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
   c->n_clusters = nc;
   c->grid = nc * C;
 
@@ -907,6 +913,9 @@ int nfb_set_option(nfb_ctx* c, int option, int value) {
     }
   } else if (option == NFB_OPT_DYNAMIC_MLP) {
     c->dyn_mlp = value ? 1 : 0;
+  } else if (option == NFB_OPT_PREFETCH_KB) {
+    if (value < 0 || value > 65536) return fail(NFB_EINVAL, "prefetch lead must be in [0, 65536] KiB");
+    c->pf_ahead = value * 1024;
   } else {
     return fail(NFB_EINVAL, "unknown option");
   }

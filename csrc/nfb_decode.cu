@@ -65,6 +65,7 @@ struct Smem {
   float* red_in;
   float* fold;
   float2* rope;   // (cos, sin) of this step's position, rd/2 entries
+  float* ubias;   // up biases of this CTA's static MLP rows (kMaxBias)
   int* misc;
   int attst_stride;
   int wst_stride;
@@ -88,9 +89,57 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, cons
   s.fold = reinterpret_cast<float*>(base + L.fold);
   s.rope = reinterpret_cast<float2*>(base + L.rope);
   s.misc = reinterpret_cast<int*>(base + L.misc);
+  s.ubias = reinterpret_cast<float*>(base + L.ubias);
   s.attst_stride = align_up(p.d + 2, 4);
   s.wst_stride = align_up(p.d + 2, 4);
   return s;
+}
+
+// ===========================================================================
+// Static, byte-balanced MLP split (computed by the 32 lanes of the producer
+// warp).  Every CTA evaluates the same formula, so the split-K partial of each
+// CTA (and the fold) is bitwise reproducible run to run.  CTA g gets chunks
+// [start_g, start_{g+1}) with start_g proportional to the prefix of
+// max(0, T - headbytes_j), T = (all bytes of the layer) / G.
+// ===========================================================================
+__device__ __forceinline__ long long head_stage_bytes(const Params& p, int k, int r, int pos) {
+  if (k >= p.H) return 0;
+  const int nh = (p.H - k + p.n_clusters - 1) / p.n_clusters;
+  const int cnt = pos / p.C + (r < pos % p.C ? 1 : 0);
+  const long long b = (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
+  return b * p.head_weight_pct / 100;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void mlp_range_warp(const Params& p, int pos, uint32_t rank, uint32_t cid, int lane,
+                                               int& c0, int& c1) {
+  const int G = p.n_clusters * p.C;
+  const long long n_ch = (p.m + p.stage_rows - 1) / p.stage_rows;
+  const long long chunk_b = 2ll * p.stage_rows * p.h * 2;
+  long long hb = 0;
+  for (int g = lane; g < G; g += 32) hb += head_stage_bytes(p, g / p.C, g % p.C, pos);
+  const long long T = (n_ch * chunk_b + warp_sum_ll(hb)) / G;
+  const int me = (int)(cid * p.C + rank);
+  long long w_all = 0, w_before = 0;
+  for (int g = lane; g < G; g += 32) {
+    const long long w = max(0ll, T - head_stage_bytes(p, g / p.C, g % p.C, pos));
+    w_all += w;
+    if (g < me) w_before += w;
+  }
+  const long long W = warp_sum_ll(w_all), cum = warp_sum_ll(w_before);
+  const long long mine = max(0ll, T - head_stage_bytes(p, (int)cid, (int)rank, pos));
+  if (W <= 0) {
+    c0 = 0;
+    c1 = me == 0 ? (int)n_ch : 0;
+    return;
+  }
+  c0 = (int)(n_ch * cum / W);
+  c1 = (int)(n_ch * (cum + mine) / W);
 }
 
 // ===========================================================================
@@ -104,10 +153,31 @@ struct Producer {
   uint64_t pol;
   unsigned long long wait_ns = 0;
 
-  __device__ __forceinline__ Producer(const Params& p_, const Smem& s_) : p(p_), s(s_) { pol = policy_evict_first(); }
+  // L2 prefetcher mode: walk the identical stage schedule, issuing
+  // cp.async.bulk.prefetch.L2 instead of ring copies, at most p.pf_ahead
+  // bytes ahead of the ring producer.  HBM keeps streaming (into L2) while
+  // the ring is full because consumers sit in a cluster / grid rendezvous.
+  const bool pf;
+  uint32_t cum16 = 0;  // bytes issued so far / 16
+  volatile uint32_t* shared_cum16;
+
+  __device__ __forceinline__ Producer(const Params& p_, const Smem& s_, bool prefetcher = false)
+      : p(p_), s(s_), pf(prefetcher) {
+    pol = policy_evict_first();
+    shared_cum16 = reinterpret_cast<volatile uint32_t*>(s.misc + kMiscCum);
+  }
 
   __device__ __forceinline__ void push(int type, int a, int n, int flags, const void* src0, uint32_t b0,
                        const void* src1 = nullptr, uint32_t b1 = 0) {
+    if (pf) {
+      const uint32_t need = cum16 + ((b0 + b1) >> 4);
+      const uint32_t ahead = (uint32_t)p.pf_ahead >> 4;
+      while (need > *shared_cum16 + ahead) __nanosleep(256);
+      if (b0) bulk_prefetch_l2(src0, b0);
+      if (b1) bulk_prefetch_l2(src1, b1);
+      cum16 = need;
+      return;
+    }
     const int slot = pslot;
     const uint32_t ph = pphase ^ 1u;
     if (p.trace) {
@@ -120,62 +190,26 @@ struct Producer {
     s.desc[slot] = Desc{type, a, n, flags};
     const uint32_t bytes = b0 + b1;
     unsigned char* dst = s.ring + (size_t)slot * p.slot_bytes;
-    if (bytes) {
+    if (bytes && !(p.debug & DBG_NO_COPY)) {
       mbar_arrive_expect_tx(&s.full[slot], bytes);
       bulk_g2s(dst, src0, b0, &s.full[slot], pol);
       if (b1) bulk_g2s(dst + b0, src1, b1, &s.full[slot], pol);
     } else {
       mbar_arrive(&s.full[slot]);
     }
+    cum16 += bytes >> 4;
+    *shared_cum16 = cum16;
     if (++pslot == p.n_slots) {
       pslot = 0;
       pphase ^= 1u;
     }
   }
 
-  int mlp_c0 = 0, mlp_c1 = 0;
-
-  // Head-stage bytes of CTA (cluster k, rank r) at history length pos.
-  __device__ __forceinline__ long long head_bytes(int k, int r, int pos) const {
-    if (k >= p.H) return 0;
-    const int nh = (p.H - k + p.n_clusters - 1) / p.n_clusters;
-    const int cnt = pos / p.C + (r < pos % p.C ? 1 : 0);
-    const long long b = (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
-    return b * p.head_weight_pct / 100;
-  }
-
-  // Static, byte-balanced MLP chunk ranges: every CTA evaluates the same
-  // formula, so the split-K partial of each CTA (and the fold) is bitwise
-  // reproducible run to run.  CTA g gets chunks [start_g, start_{g+1}) with
-  // start_g proportional to the prefix of max(0, T - headbytes_j).
-  __device__ __forceinline__ void mlp_range(int pos, uint32_t rank, uint32_t cid) {
-    const int G = p.n_clusters * p.C;
-    const long long n_ch = (p.m + p.stage_rows - 1) / p.stage_rows;
-    const long long chunk_b = 2ll * p.stage_rows * p.h * 2;
-    long long total = n_ch * chunk_b;
-    for (int g = 0; g < G; ++g) total += head_bytes(g / p.C, g % p.C, pos);
-    const long long T = total / G;
-    long long W = 0, cum = 0;
-    const int me = (int)(cid * p.C + rank);
-    for (int g = 0; g < G; ++g) {
-      const long long w = max(0ll, T - head_bytes(g / p.C, g % p.C, pos));
-      if (g == me) cum = W;
-      W += w;
-    }
-    const long long mine = max(0ll, T - head_bytes((int)cid, (int)rank, pos));
-    if (W <= 0) {
-      mlp_c0 = mlp_c1 = (me == 0) ? 0 : (int)n_ch;
-      if (me == 0) mlp_c1 = (int)n_ch;
-      return;
-    }
-    mlp_c0 = (int)(n_ch * cum / W);
-    mlp_c1 = (int)(n_ch * (cum + mine) / W);
-  }
+  int mlp_c0 = 0, mlp_c1 = 0;  // static MLP chunk range (mlp_range_warp)
 
   __device__ __forceinline__ void run(int pos, int par, uint32_t rank, uint32_t cid) {
     const int h = p.h, d = p.d, C = p.C;
     const uint32_t rowb = (uint32_t)h * 2u;
-    if (!p.dyn_mlp) mlp_range(pos, rank, cid);
     for (int l = p.l0; l < p.l1; ++l) {
       const LayerW& W = p.layers[l];
       const int lrel = l - p.l0;
@@ -210,6 +244,7 @@ struct Producer {
         }
       }
       if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
+      if (pf && p.dyn_mlp) return;  // dynamic chunk grabs cannot be replayed
       // MLP chunks in pairs: UP(c), UP(c+1) [flush], DOWN(c), DOWN(c+1), so
       // consumers do one cross-warp reduction per 2 chunks.
       int* ctr = p.ctr + par * p.ctr_stride + lrel;
@@ -240,6 +275,7 @@ struct Producer {
       }
       push(ST_END, 0, 0, 0, nullptr, 0);
     }
+    if (pf) return;
     if (p.head_mode != HEAD_NONE) {
       int* ctr = p.ctr + par * p.ctr_stride + (p.l1 - p.l0);
       for (;;) {
@@ -351,8 +387,13 @@ __device__ __forceinline__ float fast_exp2(float x) {
 
 __device__ __forceinline__ float gelu_f(float x, int exact) {
   if (exact) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+  // tanh on the MUFU (tanh.approx.f32, max rel. error ~2^-11): the paper's
+  // "PTX-accelerated GELU"; well inside the 2e-2 parity bar.
   const float k = 0.79788456080286536f;  // sqrt(2/pi)
-  return 0.5f * x * (1.0f + tanhf(k * (x + 0.044715f * x * x * x)));
+  const float u = k * fmaf(0.044715f * x, x * x, x);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.0f + t);
 }
 
 __device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
@@ -386,18 +427,20 @@ struct Consumer {
   const bool act;   // owns a live hidden chunk
   const int col;    // 16-byte column this thread reads from a weight row (0 if !act)
   const int rowb;   // bytes per weight row (hidden * 2)
+  const uint32_t ring_s;  // shared-window address of the stage ring
   bool kv_first = false;
   int pend = 0;        // rows accumulated in the current row-dot batch
   int gbuf = 0;        // wred double-buffer of MLP / LM batches
   float qbias = 0.f;   // this thread's QKV bias (row tid of this rank's QKV rows)
-  float gbias = 0.f;   // up bias of batch row `lane`
+  int grow = 0;        // up row of batch lane `lane`
+  int ub0 = 0, ubn = 0;  // up biases of rows [ub0, ub0 + ubn) staged in s.ubias this layer
   int lm_a0 = 0, lm_n0 = 0, lm_a1 = 0;
   unsigned long long kv_ns = 0, kvwait_ns = 0;
   int slot = 0;     // ring position of the next stage
   uint32_t phase = 0;
   int n_qkv = 0, n_att = 0, n_red = 0, n_events = 0;
   // registers
-  float xn1[8], xn2[8], acc[8];
+  float2 xn1[4], xn2[4], acc2[4];  // LN1(x), LN2(x), split-K accumulator (8 hidden elems)
   float gval = 0.f;                      // gelu(up) for row `lane` of the last UP stage
   // attention state (valid lanes of a position group)
   float qr[DPL], o[DPL], am, al;
@@ -408,7 +451,7 @@ struct Consumer {
                       int pos_, int step_)
       : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(p_.ncw * 32),
         rank(rank_), cid(cid_), pos(pos_), step(step_), par(step_ & 1),
-        act(tid_ < (p_.h >> 3)), col(tid_ < (p_.h >> 3) ? tid_ : 0), rowb(p_.h * 2) {}
+        act(tid_ < (p_.h >> 3)), col(tid_ < (p_.h >> 3) ? tid_ : 0), rowb(p_.h * 2), ring_s(smem_u32(s_.ring)) {}
 
   __device__ __forceinline__ void advance() {
     if (++slot == p.n_slots) {
@@ -442,7 +485,7 @@ struct Consumer {
   }
 
   // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40)
-  __device__ __forceinline__ void layer_norm(const float* x, const float* g, const float* b, float* out) {
+  __device__ __forceinline__ void layer_norm(const float* x, const float* g, const float* b, float2 (&out)[4]) {
     float sm = 0.f;
     if (act)
 #pragma unroll
@@ -462,10 +505,12 @@ struct Consumer {
       const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
       const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = (x[i] - mu) * rstd * gg[i] + bb[i];
+      for (int i = 0; i < 4; ++i)
+        out[i] = make_float2((x[2 * i] - mu) * rstd * gg[2 * i] + bb[2 * i],
+                             (x[2 * i + 1] - mu) * rstd * gg[2 * i + 1] + bb[2 * i + 1]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = 0.f;
+      for (int i = 0; i < 4; ++i) out[i] = make_float2(0.f, 0.f);
     }
   }
 
@@ -483,23 +528,25 @@ struct Consumer {
 
   // All kRows rows of this thread's 16-byte column, issued back to back
   // (rows >= n read as zero; inactive threads read column 0 and are masked by
-  // zero inputs / never store their accumulators).
-  __device__ __forceinline__ void load_rows(const unsigned char* sl, int n, uint4 (&w)[kRows]) const {
-    const unsigned char* b = sl + col * 16;
+  // zero inputs / never store their accumulators).  Addresses are 32-bit
+  // shared-window offsets (ld.shared), so no generic->shared conversion.
+  __device__ __forceinline__ void load_rows(uint32_t sl, int n, uint4 (&w)[kRows]) const {
+    const uint32_t b = sl + (uint32_t)col * 16u;
+    if (n == kRows) {
 #pragma unroll
-    for (int r = 0; r < kRows; ++r)
-      w[r] = (r < n) ? *reinterpret_cast<const uint4*>(b + r * rowb) : make_uint4(0u, 0u, 0u, 0u);
+      for (int r = 0; r < kRows; ++r) w[r] = lds128(b + (uint32_t)(r * rowb));
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) w[r] = (r < n) ? lds128(b + (uint32_t)(r * rowb)) : make_uint4(0u, 0u, 0u, 0u);
+    }
   }
 
   // Row-dot of the stage's rows with `xv`: the warp sum of row r lands in
   // wbase[r * ncw + warp] (combine across warps with row_total after a
   // consumer barrier).
-  __device__ __forceinline__ void rowdot_stage(const unsigned char* sl, int n, const float* xv, float* wbase) {
+  __device__ __forceinline__ void rowdot_stage(uint32_t sl, int n, const float2 (&x2)[4], float* wbase) {
     uint4 w[kRows];
     load_rows(sl, n, w);
-    float2 x2[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) x2[i] = make_float2(xv[2 * i], xv[2 * i + 1]);
     float v[kRows];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) v[r] = dot8x2(w[r], x2);
@@ -520,23 +567,15 @@ struct Consumer {
 
   // acc += coef[r] * row r over the stage's rows (transposed projections);
   // coef[r] must be 0 for r >= n.
-  __device__ __forceinline__ void rowacc_stage(const unsigned char* sl, int n, const float (&coef)[kRows]) {
+  __device__ __forceinline__ void rowacc_stage(uint32_t sl, int n, const float (&coef)[kRows]) {
     uint4 w[kRows];
     load_rows(sl, n, w);
-    float2 a2[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a2[i] = make_float2(acc[2 * i], acc[2 * i + 1]);
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
       const __half2* hp = reinterpret_cast<const __half2*>(&w[r]);
       const float2 c2 = make_float2(coef[r], coef[r]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a2[i] = ffma2(c2, __half22float2(hp[i]), a2[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      acc[2 * i] = a2[i].x;
-      acc[2 * i + 1] = a2[i].y;
+      for (int i = 0; i < 4; ++i) acc2[i] = ffma2(c2, __half22float2(hp[i]), acc2[i]);
     }
   }
 
@@ -808,8 +847,8 @@ struct Consumer {
       if (rank != 0) {
         if (act) {
           const uint32_t dst = mapa(smem_u32(s.red_in + (size_t)(rank - 1) * h + tid * 8), 0);
-          st_cluster_v4(dst, acc[0], acc[1], acc[2], acc[3]);
-          st_cluster_v4(dst + 16, acc[4], acc[5], acc[6], acc[7]);
+          st_cluster_v4(dst, acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y);
+          st_cluster_v4(dst + 16, acc2[2].x, acc2[2].y, acc2[3].x, acc2[3].y);
         }
         consumer_sync(nct);
         if (tid == 0) mbar_arrive_cluster(s.bar_red, 0);
@@ -819,16 +858,16 @@ struct Consumer {
           for (int r = 1; r < p.C; ++r) {
             const float4 a = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8);
             const float4 b = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8 + 4);
-            acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-            acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+            acc2[0].x += a.x; acc2[0].y += a.y; acc2[1].x += a.z; acc2[1].y += a.w;
+            acc2[2].x += b.x; acc2[2].y += b.y; acc2[3].x += b.z; acc2[3].y += b.w;
           }
       }
       ++n_red;
     }
     if (rank == 0 && act) {
       float4* dst = reinterpret_cast<float4*>(p.part + (size_t)cid * h + tid * 8);
-      __stcg(dst, make_float4(acc[0], acc[1], acc[2], acc[3]));
-      __stcg(dst + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+      __stcg(dst, make_float4(acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y));
+      __stcg(dst + 1, make_float4(acc2[2].x, acc2[2].y, acc2[3].x, acc2[3].y));
     }
     // the fold's non-partial terms (x, biases) do not depend on the barrier:
     // fetch them now so their latency hides under it
@@ -916,7 +955,7 @@ struct Consumer {
     consumer_sync(nct);
     stamp_layer(lrel, 5);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.f, 0.f);
   }
 
   // ---- main loop --------------------------------------------------------------
@@ -945,17 +984,25 @@ struct Consumer {
       } else {
         load_vec(p.xs + (size_t)lrel * h, x);
       }
+      // this CTA's up biases (static MLP range) -> smem; read at the FLUSH
+      // points after a consumer barrier (the first one follows the LNs)
+      if (!p.dyn_mlp) {
+        ub0 = s.misc[3] * p.stage_rows;
+        ubn = min(min(s.misc[4] * p.stage_rows, p.m) - ub0, kMaxBias);
+        for (int i = tid; i < ubn; i += nct) s.ubias[i] = __ldg(W.bup + ub0 + i);
+      }
       layer_norm(x, W.ln1g, W.ln1b, xn1);
       if (p.parallel) layer_norm(x, W.ln2g, W.ln2b, xn2);
       stamp_layer(lrel, 0);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.f, 0.f);
 
       for (;;) {
         const int sl = slot;
         wait_full(sl, 20);
         const Desc dsc = s.desc[sl];
         const unsigned char* buf = s.ring + (size_t)sl * p.slot_bytes;
+        const uint32_t sbuf = ring_s + (uint32_t)(sl * p.slot_bytes);
         advance();
         const int head = dsc.flags >> 8;
         const bool last = dsc.flags & F_LAST;
@@ -965,7 +1012,7 @@ struct Consumer {
             pend = 0;
             qbias = tid < p.rows_qkv ? __ldg(W.bqkv + head * 3 * p.d + (int)rank * p.rows_qkv + tid) : 0.f;
           }
-          rowdot_stage(buf, dsc.n, xn1, s.wred + pend * p.ncw);
+          if (!(p.debug & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
           release(sl);
           pend += dsc.n;
           if (last) {
@@ -983,7 +1030,7 @@ struct Consumer {
           }
         } else if (dsc.type == ST_KV) {
           const unsigned long long ta = (p.trace && tid == 0) ? globaltimer() : 0ull;
-          attention_stage(buf, dsc.n);
+          if (!(p.debug & DBG_NO_COMPUTE)) attention_stage(buf, dsc.n);
           release(sl);
           if (p.trace && tid == 0) {
             kv_ns += globaltimer() - ta;
@@ -1001,19 +1048,21 @@ struct Consumer {
           float c[kRows];
 #pragma unroll
           for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? s.ctx[dsc.a + r] : 0.f;
-          rowacc_stage(buf, dsc.n, c);
+          if (!(p.debug & DBG_NO_COMPUTE)) rowacc_stage(sbuf, dsc.n, c);
           release(sl);
         } else if (dsc.type == ST_UP) {
           if (dsc.flags & F_FIRST) pend = 0;
-          if (lane >= pend && lane < pend + dsc.n) gbias = __ldg(W.bup + dsc.a + lane - pend);
+          if (lane >= pend && lane < pend + dsc.n) grow = dsc.a + lane - pend;
           float* wb = s.wred + (gbuf * 2 * kRows + pend) * p.ncw;
-          rowdot_stage(buf, dsc.n, xn2, wb);
+          if (!(p.debug & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn2, wb);
           release(sl);
           pend += dsc.n;
           if (dsc.flags & F_FLUSH) {
             consumer_sync(nct);
             const float* wr = s.wred + (gbuf * 2 * kRows + lane) * p.ncw;
-            gval = lane < pend ? gelu_f(row_total(wr) + gbias, p.gelu_exact) : 0.f;
+            const int bi = grow - ub0;
+            const float gb = (bi >= 0 && bi < ubn) ? s.ubias[bi] : __ldg(W.bup + grow);
+            gval = lane < pend ? gelu_f(row_total(wr) + gb, p.gelu_exact) : 0.f;
             gbuf ^= 1;
           }
         } else if (dsc.type == ST_DOWN) {
@@ -1023,7 +1072,7 @@ struct Consumer {
           for (int r = 0; r < kRows; ++r) c[r] = __shfl_sync(0xffffffffu, gval, (off + r) & 31);
 #pragma unroll
           for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? c[r] : 0.f;
-          rowacc_stage(buf, dsc.n, c);
+          if (!(p.debug & DBG_NO_COMPUTE)) rowacc_stage(sbuf, dsc.n, c);
           release(sl);
         } else if (dsc.type == ST_SYNC) {
           release(sl);
@@ -1061,13 +1110,13 @@ struct Consumer {
       layer_norm(x, p.head.lnfg, p.head.lnfb, xn1);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) xn1[i] = x[i];
+      for (int i = 0; i < 4; ++i) xn1[i] = make_float2(x[2 * i], x[2 * i + 1]);
     }
     for (;;) {
       const int sl = slot;
       wait_full(sl, 21);
       const Desc dsc = s.desc[sl];
-      const unsigned char* buf = s.ring + (size_t)sl * p.slot_bytes;
+      const uint32_t sbuf = ring_s + (uint32_t)(sl * p.slot_bytes);
       advance();
       if (dsc.type == ST_LM) {
         if (dsc.flags & F_FIRST) {
@@ -1077,7 +1126,7 @@ struct Consumer {
         } else {
           lm_a1 = dsc.a;
         }
-        rowdot_stage(buf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * p.ncw);
+        if (!(p.debug & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * p.ncw);
         release(sl);
         pend += dsc.n;
         if (dsc.flags & F_FLUSH) {
@@ -1142,6 +1191,7 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
       if (tok < 0 || tok >= p.V) tok = 0;
     }
     s.misc[2] = tok;
+    s.misc[kMiscCum] = 0;
     if (blockIdx.x == 0) {
       // Slots of the other parity are idle during this launch: reset them.
       for (int i = 0; i < p.ctr_stride; ++i) p.ctr[(par ^ 1) * p.ctr_stride + i] = 0;
@@ -1154,13 +1204,23 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
     const int half = p.rd >> 1;
     for (int i = tid; i < half; i += blockDim.x) s.rope[i] = __ldg(&p.rope[(size_t)s.misc[0] * half + i]);
   }
+  const int warp = tid >> 5;
+  if (warp == p.ncw) {
+    int c0 = 0, c1 = 0;
+    if (!p.dyn_mlp) mlp_range_warp(p, s.misc[0], rank, cid, tid & 31, c0, c1);
+    if ((tid & 31) == 0) {
+      s.misc[3] = c0;
+      s.misc[4] = c1;
+    }
+  }
   cluster_sync_all();
   const int pos = s.misc[0], step = s.misc[1];
 
-  const int warp = tid >> 5;
-  if (warp == p.ncw) {
+  if (warp == p.ncw || (warp == p.ncw + 1 && p.pf_ahead > 0)) {
     if ((tid & 31) == 0) {
-      Producer prod(p, s);
+      Producer prod(p, s, warp != p.ncw);
+      prod.mlp_c0 = s.misc[3];
+      prod.mlp_c1 = s.misc[4];
       prod.run(pos, step & 1, rank, cid);
     }
   } else if (warp < p.ncw) {
@@ -1171,9 +1231,9 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
 }
 
 // Explicit instantiations used by the host launcher: 8 head dims per lane,
-// block of <= 12 warps (hidden <= 2816) or <= 17 warps (hidden <= 4096).
+// block of <= 12 warps (hidden <= 2560) or <= 18 warps (hidden <= 4096).
 template __global__ void decode_kernel<8, 384>(const Params);
-template __global__ void decode_kernel<8, 544>(const Params);
+template __global__ void decode_kernel<8, 576>(const Params);
 
 }  // namespace nfb
 
@@ -1182,10 +1242,10 @@ template __global__ void decode_kernel<8, 544>(const Params);
 // ===========================================================================
 namespace nfb {
 
-// `variant`: 0 -> block <= 384 threads, 1 -> block <= 544 threads.
+// `variant`: 0 -> block <= 384 threads, 1 -> block <= 576 threads.
 const void* decode_kernel_ptr(int variant) {
   return variant == 0 ? reinterpret_cast<const void*>(&decode_kernel<8, 384>)
-                      : reinterpret_cast<const void*>(&decode_kernel<8, 544>);
+                      : reinterpret_cast<const void*>(&decode_kernel<8, 576>);
 }
 
 cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
@@ -1209,7 +1269,7 @@ cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int sme
   cfg.attrs = at;
   cfg.numAttrs = na;
   if (dpl == 0) return cudaLaunchKernelEx(&cfg, decode_kernel<8, 384>, p);
-  return cudaLaunchKernelEx(&cfg, decode_kernel<8, 544>, p);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<8, 576>, p);
 }
 
 cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out) {

@@ -8,6 +8,8 @@ namespace nfb {
 
 // Weight stages carry at most this many matrix rows.
 constexpr int kRows = 8;
+// Up biases staged in shared memory per layer (static MLP split).
+constexpr int kMaxBias = 512;
 // Upper bound on consumer warps (hidden <= 16 * 256 = 4096).
 constexpr int kMaxConsumerWarps = 16;
 
@@ -64,6 +66,8 @@ struct Params {
   int advance_pos;      // graph/decode mode: pos += 1 after the step
   int dyn_mlp;          // 1: MLP chunks grabbed dynamically (not bitwise reproducible)
   int head_weight_pct;  // static schedule: head-stage bytes weighted by this / 100
+  int pf_ahead;         // L2 prefetcher lead over the ring producer (bytes); 0 = off
+  int debug;            // DBG_* bits (measurement only: results are garbage)
   // pointers
   const LayerW* layers;
   HeadW head;
@@ -92,9 +96,18 @@ struct Params {
 constexpr int kTraceHeader = 8;
 constexpr int kTracePerLayer = 12;
 
+// Measurement-only modes (NFB_DEBUG env): stages arrive without data, or
+// consumers skip the arithmetic.  Used to split producer- vs consumer-bound time.
+constexpr int DBG_NO_COPY = 1;
+constexpr int DBG_NO_COMPUTE = 2;
+
+// misc[] word holding the ring producer's issued bytes / 16 (read by the
+// L2 prefetcher warp).
+constexpr int kMiscCum = 56;
+
 // Shared-memory carve-up, computed identically on host and device.
 struct Layout {
-  int ring, full, empty, desc, bars, ybuf, attst, ctx, wst, wred, red_in, fold, rope, misc, total;
+  int ring, full, empty, desc, bars, ybuf, attst, ctx, wst, wred, red_in, fold, rope, misc, ubias, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -117,6 +130,7 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.fold = o;   o += 4 * 32 * p.ncw;
   L.rope = o;   o += 4 * align_up(p.rd, 4);
   L.misc = o;   o += 4 * 64;
+  L.ubias = o;  o += 4 * kMaxBias;
   L.total = align_up(o, 128);
   return L;
 }

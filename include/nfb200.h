@@ -141,9 +141,10 @@ int nfb_read_logits(nfb_ctx* ctx, float* out);
 int nfb_get_state(nfb_ctx* ctx, int* pos, int* step);
 /* Options: NFB_OPT_TRACE (per-CTA globaltimer phase stamps, see
  * csrc/nfb_internal.h), NFB_OPT_DYNAMIC_MLP (work-stealing MLP chunks: not
- * bitwise reproducible).  Invalidates a captured graph. */
+ * bitwise reproducible), NFB_OPT_PREFETCH_KB.  Invalidates a captured graph. */
 #define NFB_OPT_TRACE 1
 #define NFB_OPT_DYNAMIC_MLP 2
+#define NFB_OPT_PREFETCH_KB 3 /* L2 prefetch lead of the prefetcher warp, KiB (0 = off) */
 int nfb_set_option(nfb_ctx* ctx, int option, int value);
 /* Copy up to n trace words ([grid][8 + 12*n_layers]) to `out`. */
 int nfb_read_trace(nfb_ctx* ctx, unsigned long long* out, int n);

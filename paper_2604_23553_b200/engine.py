@@ -238,9 +238,12 @@ class Engine:
         check(self.lib.nfb_get_state(self._h, C.byref(pos), C.byref(step)), "nfb_get_state")
         return pos.value, step.value
 
-    def set_option(self, option: str, value: bool) -> None:
-        code = {"trace": _lib.OPT_TRACE, "dynamic_mlp": _lib.OPT_DYNAMIC_MLP}[option]
-        check(self.lib.nfb_set_option(self._h, code, int(bool(value))), "nfb_set_option")
+    def set_option(self, option: str, value) -> None:
+        """"trace" / "dynamic_mlp" (bool) or "prefetch_kb" (int, L2 prefetch lead)."""
+        code = {"trace": _lib.OPT_TRACE, "dynamic_mlp": _lib.OPT_DYNAMIC_MLP,
+                "prefetch_kb": _lib.OPT_PREFETCH_KB}[option]
+        v = int(value) if option == "prefetch_kb" else int(bool(value))
+        check(self.lib.nfb_set_option(self._h, code, v), "nfb_set_option")
 
     def read_trace(self) -> np.ndarray:
         """Per-CTA phase stamps of the last launch: [grid, 8 + 12*n_layers] (ns)."""
