@@ -113,7 +113,8 @@ __device__ __forceinline__ double synth_value(int kind, double u, double div) {
   }
 }
 
-// out[i] (or out[transposed i]) = fp16(synth(kind, uniform(seed, stream, i)))
+// out[layout(i)] = fp16(synth(kind, uniform(seed, stream, i))); layout 0 row-major,
+// 1 transposed, 2 8-row blocked (blk8_index)
 __global__ void synth_kernel(uint64_t seed, uint32_t stream, uint64_t n, int kind, double div,
                              uint16_t* out16, float* out32, int64_t rows, int64_t cols,
                              int transpose) {
@@ -121,7 +122,8 @@ __global__ void synth_kernel(uint64_t seed, uint32_t stream, uint64_t n, int kin
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint16_t hb = f64_to_f16_bits(synth_value(kind, uniform(seed, stream, i), div));
     uint64_t idx = i;
-    if (transpose) idx = (i % (uint64_t)cols) * (uint64_t)rows + i / (uint64_t)cols;
+    if (transpose == 1) idx = (i % (uint64_t)cols) * (uint64_t)rows + i / (uint64_t)cols;
+    else if (transpose == 2) idx = blk8_index(i / (uint64_t)cols, i % (uint64_t)cols, (size_t)cols);
     if (out16) out16[idx] = hb;
     else out32[idx] = f16_bits_to_f32(hb);
   }
@@ -166,7 +168,7 @@ struct nfb_ctx {
   nfb_model_desc desc{};
   int device = 0;
   int max_seq = 0;
-  int C = 2, n_clusters = 0, grid = 0, ncw = 0, block = 0, dpl = 16;
+  int C = 2, n_clusters = 0, grid = 0, ncw = 0, block = 0, dpl = 0;  // dpl: kernel variant
   int stage_rows = 8, slot_bytes = 0, n_slots = 0, kv_pos = 0, smem = 0, sm_count = 0;
   bool coop = true;
   cudaStream_t stream = nullptr;
@@ -194,6 +196,7 @@ struct nfb_ctx {
   int head_weight_pct = 130;
   int debug = 0;
   int pf_ahead = 0;  // L2 prefetcher lead (bytes); measured: no gain at C2
+  int mlp_gap = 1;   // MLP pairs interleaved into the head schedule (split-phase cluster syncs)
   unsigned long long* h_tok = nullptr;  // pinned [2]
   std::vector<void*> allocs;
 };
@@ -261,6 +264,7 @@ Params base_params(nfb_ctx* c) {
   p.dyn_mlp = c->dyn_mlp;
   p.head_weight_pct = c->head_weight_pct;
   p.pf_ahead = c->pf_ahead;
+  p.mlp_gap = c->mlp_gap;
   p.debug = c->debug;
   return p;
 }
@@ -305,13 +309,21 @@ int to_f16_host(const void* src, int dtype, size_t n, std::vector<uint16_t>& out
   return NFB_OK;
 }
 
-int upload_f16(const void* src, int dtype, size_t rows, size_t cols, bool transpose, uint16_t* dst) {
+enum Layout2D : int { L_ROW = 0, L_TRANSPOSED = 1, L_BLK8 = 2 };
+
+size_t layout_index(int layout, size_t r, size_t k, size_t rows, size_t cols) {
+  if (layout == L_TRANSPOSED) return k * rows + r;
+  if (layout == L_BLK8) return blk8_index(r, k, cols);
+  return r * cols + k;
+}
+
+int upload_f16(const void* src, int dtype, size_t rows, size_t cols, int layout, uint16_t* dst) {
   std::vector<uint16_t> h;
   TRY(to_f16_host(src, dtype, rows * cols, h));
-  if (transpose) {
+  if (layout != L_ROW) {
     std::vector<uint16_t> t(rows * cols);
     for (size_t r = 0; r < rows; ++r)
-      for (size_t k = 0; k < cols; ++k) t[k * rows + r] = h[r * cols + k];
+      for (size_t k = 0; k < cols; ++k) t[layout_index(layout, r, k, rows, cols)] = h[r * cols + k];
     h.swap(t);
   }
   CK(cudaMemcpy(dst, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
@@ -362,7 +374,8 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
     return fail(NFB_EUNSUPPORTED, "hidden must be a multiple of 8 and <= 4096");
   if (m.d_head % 8) return fail(NFB_EUNSUPPORTED, "d_head must be a multiple of 8");
   if (max_seq < 1) return fail(NFB_EINVAL, "max_seq must be >= 1");
-  const int C = cluster_size > 0 ? cluster_size : 2;
+  int C = cluster_size > 0 ? cluster_size : 2;
+  if (cluster_size <= 0 && getenv("NFB_CLUSTER")) C = atoi(getenv("NFB_CLUSTER"));
   if (C > 8 || (3 * m.d_head) % C || m.d_head % C)
     return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8 and divide d_head");
 
@@ -413,6 +426,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (getenv("NFB_HEAD_WEIGHT")) c->head_weight_pct = atoi(getenv("NFB_HEAD_WEIGHT"));
   if (getenv("NFB_DEBUG")) c->debug = atoi(getenv("NFB_DEBUG"));
   if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
+  if (getenv("NFB_MLP_GAP")) c->mlp_gap = atoi(getenv("NFB_MLP_GAP"));
   c->n_clusters = nc;
   c->grid = nc * C;
 
@@ -527,15 +541,15 @@ int nfb_set_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w, int
   LayerBufs& b = c->layers[layer];
   TRY(upload_f32_of_f16(w->ln1_gain, dtype, h, b.ln1g));
   TRY(upload_f32_of_f16(w->ln1_bias, dtype, h, b.ln1b));
-  TRY(upload_f16(w->qkv_weight, dtype, (size_t)3 * h, h, false, b.wqkv));
+  TRY(upload_f16(w->qkv_weight, dtype, (size_t)3 * h, h, L_ROW, b.wqkv));
   TRY(upload_f32_of_f16(w->qkv_bias, dtype, (size_t)3 * h, b.bqkv));
-  TRY(upload_f16(w->out_weight, dtype, h, h, true, b.woT));
+  TRY(upload_f16(w->out_weight, dtype, h, h, L_TRANSPOSED, b.woT));
   TRY(upload_f32_of_f16(w->out_bias, dtype, h, b.bo));
   TRY(upload_f32_of_f16(w->ln2_gain, dtype, h, b.ln2g));
   TRY(upload_f32_of_f16(w->ln2_bias, dtype, h, b.ln2b));
-  TRY(upload_f16(w->up_weight, dtype, m, h, false, b.wup));
+  TRY(upload_f16(w->up_weight, dtype, m, h, L_ROW, b.wup));
   TRY(upload_f32_of_f16(w->up_bias, dtype, m, b.bup));
-  TRY(upload_f16(w->down_weight, dtype, h, m, true, b.wdT));
+  TRY(upload_f16(w->down_weight, dtype, h, m, L_TRANSPOSED, b.wdT));
   TRY(upload_f32_of_f16(w->down_bias, dtype, h, b.bd));
   b.weights = true;
   return NFB_OK;
@@ -552,26 +566,25 @@ int nfb_synth_block_weights(nfb_ctx* c, int layer, uint64_t seed) {
   TRY(launch_synth(st, seed, 1, h, K_LNBIAS, 1.0, nullptr, b.ln1b));
   TRY(launch_synth(st, seed, 2, 3 * h * h, K_WEIGHT, std::sqrt((double)h), b.wqkv, nullptr));
   TRY(launch_synth(st, seed, 3, 3 * h, K_BIAS, 1.0, nullptr, b.bqkv));
-  TRY(launch_synth(st, seed, 4, h * h, K_WEIGHT, std::sqrt((double)h), b.woT, nullptr, h, h, 1));
+  TRY(launch_synth(st, seed, 4, h * h, K_WEIGHT, std::sqrt((double)h), b.woT, nullptr, h, h, L_TRANSPOSED));
   TRY(launch_synth(st, seed, 5, h, K_BIAS, 1.0, nullptr, b.bo));
   TRY(launch_synth(st, seed, 6, h, K_GAIN, 1.0, nullptr, b.ln2g));
   TRY(launch_synth(st, seed, 7, h, K_LNBIAS, 1.0, nullptr, b.ln2b));
   TRY(launch_synth(st, seed, 8, m * h, K_WEIGHT, std::sqrt((double)h), b.wup, nullptr));
   TRY(launch_synth(st, seed, 9, m, K_BIAS, 1.0, nullptr, b.bup));
-  TRY(launch_synth(st, seed, 10, h * m, K_WEIGHT, std::sqrt((double)m), b.wdT, nullptr, h, m, 1));
+  TRY(launch_synth(st, seed, 10, h * m, K_WEIGHT, std::sqrt((double)m), b.wdT, nullptr, h, m, L_TRANSPOSED));
   TRY(launch_synth(st, seed, 11, h, K_BIAS, 1.0, nullptr, b.bd));
   CK(cudaStreamSynchronize(st));
   b.weights = true;
   return NFB_OK;
 }
 
-static int read_f16(const uint16_t* src, size_t rows, size_t cols, bool transpose, void* dst) {
+static int read_f16(const uint16_t* src, size_t rows, size_t cols, int layout, void* dst) {
   std::vector<uint16_t> h(rows * cols);
   CK(cudaMemcpy(h.data(), src, h.size() * 2, cudaMemcpyDeviceToHost));
   float* o = static_cast<float*>(dst);
   for (size_t r = 0; r < rows; ++r)
-    for (size_t k = 0; k < cols; ++k)
-      o[r * cols + k] = f16_bits_to_f32(transpose ? h[k * rows + r] : h[r * cols + k]);
+    for (size_t k = 0; k < cols; ++k) o[r * cols + k] = f16_bits_to_f32(h[layout_index(layout, r, k, rows, cols)]);
   return NFB_OK;
 }
 
@@ -594,15 +607,15 @@ int nfb_read_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w) {
     if (!p) return fail(NFB_EINVAL, "every output tensor is required");
   TRY(read_f32(b.ln1g, h, o[0]));
   TRY(read_f32(b.ln1b, h, o[1]));
-  TRY(read_f16(b.wqkv, 3 * h, h, false, o[2]));
+  TRY(read_f16(b.wqkv, 3 * h, h, L_ROW, o[2]));
   TRY(read_f32(b.bqkv, 3 * h, o[3]));
-  TRY(read_f16(b.woT, h, h, true, o[4]));
+  TRY(read_f16(b.woT, h, h, L_TRANSPOSED, o[4]));
   TRY(read_f32(b.bo, h, o[5]));
   TRY(read_f32(b.ln2g, h, o[6]));
   TRY(read_f32(b.ln2b, h, o[7]));
-  TRY(read_f16(b.wup, m, h, false, o[8]));
+  TRY(read_f16(b.wup, m, h, L_ROW, o[8]));
   TRY(read_f32(b.bup, m, o[9]));
-  TRY(read_f16(b.wdT, h, m, true, o[10]));
+  TRY(read_f16(b.wdT, h, m, L_TRANSPOSED, o[10]));
   TRY(read_f32(b.bd, h, o[11]));
   return NFB_OK;
 }
@@ -613,7 +626,7 @@ int nfb_set_head(nfb_ctx* c, const void* embed, const void* lnf_gain, const void
   cudaSetDevice(c->device);
   const size_t h = c->desc.hidden, V = c->desc.vocab;
   if (embed) {
-    TRY(upload_f16(embed, dtype, V, h, false, c->embed));
+    TRY(upload_f16(embed, dtype, V, h, L_ROW, c->embed));
     c->has_embed = true;
   }
   if (lnf_gain || lnf_bias) {
@@ -623,7 +636,7 @@ int nfb_set_head(nfb_ctx* c, const void* embed, const void* lnf_gain, const void
     c->has_lnf = true;
   }
   if (unembed) {
-    TRY(upload_f16(unembed, dtype, V, h, false, c->unembed));
+    TRY(upload_f16(unembed, dtype, V, h, L_ROW, c->unembed));
     c->has_unembed = true;
   }
   return NFB_OK;
@@ -906,7 +919,7 @@ int nfb_set_option(nfb_ctx* c, int option, int value) {
   cudaSetDevice(c->device);
   if (option == NFB_OPT_TRACE) {
     if (value && !c->trace) {
-      c->trace_stride = kTraceHeader + kTracePerLayer * c->desc.n_layers;
+      c->trace_stride = kTraceHeader + kTracePerLayer * c->desc.n_layers + kTraceStageWords;
       TRY(dalloc(c, &c->trace, (size_t)c->grid * c->trace_stride));
     } else if (!value) {
       c->trace = nullptr;  // buffer stays in allocs until destroy

@@ -161,44 +161,63 @@ struct Producer {
   uint32_t cum16 = 0;  // bytes issued so far / 16
   volatile uint32_t* shared_cum16;
 
-  __device__ __forceinline__ Producer(const Params& p_, const Smem& s_, bool prefetcher = false)
-      : p(p_), s(s_), pf(prefetcher) {
+  const int lane;
+  __device__ __forceinline__ Producer(const Params& p_, const Smem& s_, int lane_, bool prefetcher = false)
+      : p(p_), s(s_), pf(prefetcher), lane(lane_) {
     pol = policy_evict_first();
     shared_cum16 = reinterpret_cast<volatile uint32_t*>(s.misc + kMiscCum);
   }
 
+  // Executed by all 32 lanes of the producer warp (no intra-warp divergence
+  // against the other lanes' end-of-kernel cluster barrier); lane 0 issues.
   __device__ __forceinline__ void push(int type, int a, int n, int flags, const void* src0, uint32_t b0,
                        const void* src1 = nullptr, uint32_t b1 = 0) {
     if (pf) {
       const uint32_t need = cum16 + ((b0 + b1) >> 4);
       const uint32_t ahead = (uint32_t)p.pf_ahead >> 4;
       while (need > *shared_cum16 + ahead) __nanosleep(256);
-      if (b0) bulk_prefetch_l2(src0, b0);
-      if (b1) bulk_prefetch_l2(src1, b1);
+      if (lane == 0) {
+        if (b0) bulk_prefetch_l2(src0, b0);
+        if (b1) bulk_prefetch_l2(src1, b1);
+      }
+      __syncwarp();
       cum16 = need;
       return;
     }
     const int slot = pslot;
     const uint32_t ph = pphase ^ 1u;
+    unsigned long long* slog = nullptr;
     if (p.trace) {
-      const unsigned long long t0 = globaltimer();
+      const unsigned long long t0 = clock64();
       mbar_wait(&s.empty[slot], ph, p.err, 10);
-      wait_ns += globaltimer() - t0;
+      wait_ns += clock64() - t0;
+      if (log_on && n_log < kTraceStageMax) {
+        if (lane == 0) {
+          slog = p.trace + (size_t)blockIdx.x * p.trace_stride + (p.trace_stride - kTraceStageWords) +
+                 kTraceStageProd + 2 * n_log;
+          slog[0] = t0;  // before the empty-slot wait
+        }
+        ++n_log;
+      }
     } else {
       mbar_wait(&s.empty[slot], ph, p.err, 10);
     }
-    s.desc[slot] = Desc{type, a, n, flags};
     const uint32_t bytes = b0 + b1;
-    unsigned char* dst = s.ring + (size_t)slot * p.slot_bytes;
-    if (bytes && !(p.debug & DBG_NO_COPY)) {
-      mbar_arrive_expect_tx(&s.full[slot], bytes);
-      bulk_g2s(dst, src0, b0, &s.full[slot], pol);
-      if (b1) bulk_g2s(dst + b0, src1, b1, &s.full[slot], pol);
-    } else {
-      mbar_arrive(&s.full[slot]);
+    if (lane == 0) {
+      s.desc[slot] = Desc{type, a, n, flags};
+      unsigned char* dst = s.ring + (size_t)slot * p.slot_bytes;
+      if (bytes && !(p.debug & DBG_NO_COPY)) {
+        mbar_arrive_expect_tx(&s.full[slot], bytes);
+        bulk_g2s(dst, src0, b0, &s.full[slot], pol);
+        if (b1) bulk_g2s(dst + b0, src1, b1, &s.full[slot], pol);
+      } else {
+        mbar_arrive(&s.full[slot]);
+      }
+      if (slog) slog[1] = clock64();
     }
+    __syncwarp();
     cum16 += bytes >> 4;
-    *shared_cum16 = cum16;
+    if (lane == 0) *shared_cum16 = cum16;
     if (++pslot == p.n_slots) {
       pslot = 0;
       pphase ^= 1u;
@@ -206,13 +225,57 @@ struct Producer {
   }
 
   int mlp_c0 = 0, mlp_c1 = 0;  // static MLP chunk range (mlp_range_warp)
+  bool log_on = false;
+  int n_log = 0;
 
+  // MLP chunks in pairs: UP(c), UP(c+1) [flush], DOWN(c), DOWN(c+1), so
+  // consumers do one cross-warp reduction per 2 chunks.  Emits at most
+  // `max_pairs` pairs (all remaining if < 0) from the static range
+  // [next, mlp_c1) or, in dynamic mode, from the shared counter.
+  __device__ __forceinline__ void emit_mlp(const LayerW& W, int* ctr, int& next, int max_pairs) {
+    const uint32_t rowb = (uint32_t)p.h * 2u;
+    for (int k = 0; max_pairs < 0 || k < max_pairs; ++k) {
+      int ca, cb;
+      if (p.dyn_mlp) {
+        ca = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctr, 1) : 0, 0);
+        if (ca * p.stage_rows >= p.m) break;
+        cb = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctr, 1) : 0, 0);
+        if (cb * p.stage_rows >= p.m) cb = -1;
+      } else {
+        if (next >= mlp_c1) break;
+        ca = next;
+        cb = next + 1 < mlp_c1 ? next + 1 : -1;
+        next += 2;
+      }
+      const int ra = ca * p.stage_rows, na = min(p.stage_rows, p.m - ra);
+      push(ST_UP, ra, na, F_FIRST | (cb < 0 ? F_FLUSH : 0), W.wup + (size_t)ra * p.h, na * rowb);
+      int rb = 0, nb = 0;
+      if (cb >= 0) {
+        rb = cb * p.stage_rows;
+        nb = min(p.stage_rows, p.m - rb);
+        push(ST_UP, rb, nb, F_FLUSH, W.wup + (size_t)rb * p.h, nb * rowb);
+      }
+      push(ST_DOWN, ra, na, 0, W.wdT + (size_t)ra * p.h, na * rowb);
+      if (cb >= 0) push(ST_DOWN, rb, nb, na << 8, W.wdT + (size_t)rb * p.h, nb * rowb);
+    }
+  }
+
+  // Stage schedule of one CTA.  Per head of its cluster: QKV rows, KV share,
+  // W_out^T rows.  With the parallel residual the MLP does not depend on the
+  // attention, so `p.mlp_gap` MLP pairs are slotted in after the QKV rows and
+  // after the KV share: consumers stream them while the cluster's QKV
+  // exchange / softmax merge completes (split-phase DSMEM barriers, see
+  // Consumer), instead of stalling the ring.
   __device__ __forceinline__ void run(int pos, int par, uint32_t rank, uint32_t cid) {
     const int h = p.h, d = p.d, C = p.C;
     const uint32_t rowb = (uint32_t)h * 2u;
+    const int gap = (p.parallel && !p.dyn_mlp) ? p.mlp_gap : 0;
     for (int l = p.l0; l < p.l1; ++l) {
       const LayerW& W = p.layers[l];
       const int lrel = l - p.l0;
+      log_on = lrel == (p.l1 - p.l0) / 2;
+      int* ctr = p.ctr + par * p.ctr_stride + lrel;
+      int next = mlp_c0;
       for (int hh = (int)cid; hh < p.H; hh += p.n_clusters) {
         const int tag = hh << 8;
         // QKV rows of this head owned by this rank.
@@ -223,6 +286,7 @@ struct Producer {
           const int first = r == 0 ? F_FIRST : 0;
           push(ST_QKV, q0 + r, n, tag | last | first, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h, n * rowb);
         }
+        if (gap) emit_mlp(W, ctr, next, gap);
         // KV history share (partition_kv: first hist % C ranks get one extra).
         const int base = pos / C, extra = pos % C;
         const int cnt = base + ((int)rank < extra ? 1 : 0);
@@ -235,6 +299,7 @@ struct Producer {
           push(ST_KV, st + q, n, tag | last, W.kc + off, (uint32_t)n * d * 2, W.vc + off,
                (uint32_t)n * d * 2);
         }
+        if (gap) emit_mlp(W, ctr, next, gap);
         // W_out^T rows (context elements) owned by this rank.
         const int o0 = (int)rank * p.rows_o;
         for (int r = 0; r < p.rows_o; r += p.stage_rows) {
@@ -245,43 +310,16 @@ struct Producer {
       }
       if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
       if (pf && p.dyn_mlp) return;  // dynamic chunk grabs cannot be replayed
-      // MLP chunks in pairs: UP(c), UP(c+1) [flush], DOWN(c), DOWN(c+1), so
-      // consumers do one cross-warp reduction per 2 chunks.
-      int* ctr = p.ctr + par * p.ctr_stride + lrel;
-      int next = mlp_c0;
-      for (;;) {
-        int ca, cb;
-        if (p.dyn_mlp) {
-          ca = atomicAdd(ctr, 1);
-          if (ca * p.stage_rows >= p.m) break;
-          cb = atomicAdd(ctr, 1);
-          if (cb * p.stage_rows >= p.m) cb = -1;
-        } else {
-          if (next >= mlp_c1) break;
-          ca = next;
-          cb = next + 1 < mlp_c1 ? next + 1 : -1;
-          next += 2;
-        }
-        const int ra = ca * p.stage_rows, na = min(p.stage_rows, p.m - ra);
-        push(ST_UP, ra, na, F_FIRST | (cb < 0 ? F_FLUSH : 0), W.wup + (size_t)ra * h, na * rowb);
-        int rb = 0, nb = 0;
-        if (cb >= 0) {
-          rb = cb * p.stage_rows;
-          nb = min(p.stage_rows, p.m - rb);
-          push(ST_UP, rb, nb, F_FLUSH, W.wup + (size_t)rb * h, nb * rowb);
-        }
-        push(ST_DOWN, ra, na, 0, W.wdT + (size_t)ra * h, na * rowb);
-        if (cb >= 0) push(ST_DOWN, rb, nb, na << 8, W.wdT + (size_t)rb * h, nb * rowb);
-      }
+      emit_mlp(W, ctr, next, -1);
       push(ST_END, 0, 0, 0, nullptr, 0);
     }
     if (pf) return;
     if (p.head_mode != HEAD_NONE) {
       int* ctr = p.ctr + par * p.ctr_stride + (p.l1 - p.l0);
       for (;;) {
-        const int ra = atomicAdd(ctr, 1) * p.stage_rows;
+        const int ra = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctr, 1) : 0, 0) * p.stage_rows;
         if (ra >= p.V) break;
-        int rb = atomicAdd(ctr, 1) * p.stage_rows;
+        int rb = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctr, 1) : 0, 0) * p.stage_rows;
         if (rb >= p.V) rb = -1;
         const int na = min(p.stage_rows, p.V - ra);
         push(ST_LM, ra, na, F_FIRST | (rb < 0 ? F_FLUSH : 0), p.head.unembed + (size_t)ra * h, na * rowb);
@@ -291,7 +329,7 @@ struct Producer {
       }
       push(ST_HEAD_END, 0, 0, 0, nullptr, 0);
     }
-    if (p.trace) p.trace[(size_t)blockIdx.x * p.trace_stride + 0] = wait_ns;
+    if (p.trace && lane == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + 0] = wait_ns;
   }
 };
 
@@ -470,9 +508,9 @@ struct Consumer {
   unsigned long long last_wait = 0;
   __device__ __forceinline__ void wait_full(int sl, int code) {
     if (p.trace && tid == 0) {
-      const unsigned long long t0 = globaltimer();
+      const unsigned long long t0 = clock64();
       mbar_wait(&s.full[sl], phase, p.err, code);
-      last_wait = globaltimer() - t0;
+      last_wait = clock64() - t0;
       wait_ns += last_wait;
     } else {
       mbar_wait(&s.full[sl], phase, p.err, code);
@@ -738,8 +776,11 @@ struct Consumer {
     m = M;
   }
 
-  // Groups -> warp -> CTA -> cluster (DSMEM) -> context vector in s.ctx.
-  __device__ __forceinline__ void attention_finish() {
+  // Groups -> warp -> CTA -> cluster (DSMEM): publishes this rank's softmax
+  // state to every rank's attst[rank] and arrives on the cluster barrier
+  // (split phase: attention_complete() waits and merges, at the first W_out
+  // stage, so MLP stages in between run while the partner rank catches up).
+  __device__ __forceinline__ void attention_publish() {
     const int T = tpp(), gpw = 32 / T, sub = lane % T;
     const int d = p.d;
     // 1) fold the warp's groups into group 0 (lanes 0..T-1)
@@ -791,6 +832,15 @@ struct Consumer {
     stamp_layer(cur_layer - p.l0, 7);
     if (tid == 0)
       for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_att, r);
+    att_pending = true;
+  }
+
+  // Second half of the softmax merge: wait for every rank's state, merge
+  // the C states in rank order (nf/golden.py:128-136) -> context in s.ctx.
+  __device__ __forceinline__ void attention_complete() {
+    if (!att_pending) return;
+    att_pending = false;
+    const int d = p.d;
     mbar_wait_cluster(s.bar_att, n_att & 1, p.err, 12);
     ++n_att;
     // 3) merge the C rank states in rank order -> context
@@ -816,11 +866,22 @@ struct Consumer {
     stamp_layer(cur_layer - p.l0, 2);
   }
 
-  // ---- QKV exchange ----------------------------------------------------------
-  __device__ __forceinline__ void qkv_exchange_done(int head) {
-    consumer_sync(nct);  // all ybuf stores of this rank issued (warp 0 wrote them)
+  // ---- QKV exchange (split phase) ---------------------------------------------
+  bool qkv_pending = false, att_pending = false;
+  int pend_head = 0;
+  __device__ __forceinline__ void qkv_publish(int head) {
+    consumer_sync(nct);  // all ybuf stores of this rank issued
     if (tid == 0)
       for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_qkv, r);
+    qkv_pending = true;
+    pend_head = head;
+  }
+
+  // Wait for every rank's QKV rows, append K/V, start the attention.
+  __device__ __forceinline__ void qkv_complete() {
+    if (!qkv_pending) return;
+    qkv_pending = false;
+    const int head = pend_head;
     mbar_wait_cluster(s.bar_qkv, n_qkv & 1, p.err, 11);
     ++n_qkv;
     stamp_layer(cur_layer - p.l0, 1);
@@ -997,10 +1058,22 @@ struct Consumer {
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.f, 0.f);
 
+      const bool log_on = p.trace && tid == 0 && lrel == (p.l1 - p.l0) / 2;
+      int n_log = 0;
       for (;;) {
         const int sl = slot;
+        unsigned long long* slog = nullptr;
+        if (log_on && n_log < kTraceStageMax) {
+          slog = p.trace + (size_t)blockIdx.x * p.trace_stride + (p.trace_stride - kTraceStageWords) + 4 * n_log++;
+          slog[0] = clock64();
+        }
         wait_full(sl, 20);
         const Desc dsc = s.desc[sl];
+        if (slog) {
+          slog[1] = clock64();
+          slog[3] = (unsigned long long)dsc.type | ((unsigned long long)dsc.n << 8) |
+                    ((unsigned long long)(unsigned)dsc.flags << 32);
+        }
         const unsigned char* buf = s.ring + (size_t)sl * p.slot_bytes;
         const uint32_t sbuf = ring_s + (uint32_t)(sl * p.slot_bytes);
         advance();
@@ -1026,14 +1099,15 @@ struct Consumer {
               const uint32_t a = smem_u32(s.ybuf + q0 + t);
               for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(a, r), y);
             }
-            qkv_exchange_done(head);
+            qkv_publish(head);
           }
         } else if (dsc.type == ST_KV) {
-          const unsigned long long ta = (p.trace && tid == 0) ? globaltimer() : 0ull;
+          qkv_complete();
+          const unsigned long long ta = (p.trace && tid == 0) ? clock64() : 0ull;
           if (!(p.debug & DBG_NO_COMPUTE)) attention_stage(buf, dsc.n);
           release(sl);
           if (p.trace && tid == 0) {
-            kv_ns += globaltimer() - ta;
+            kv_ns += clock64() - ta;
             kvwait_ns += last_wait;
           }
           if (kv_first) {
@@ -1042,9 +1116,10 @@ struct Consumer {
           }
           if (last) {
             if ((int)rank == p.C - 1) attention_new_token();
-            attention_finish();
+            attention_publish();
           }
         } else if (dsc.type == ST_WO) {
+          attention_complete();
           float c[kRows];
 #pragma unroll
           for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? s.ctx[dsc.a + r] : 0.f;
@@ -1076,12 +1151,16 @@ struct Consumer {
           release(sl);
         } else if (dsc.type == ST_SYNC) {
           release(sl);
+          qkv_complete();
+          attention_complete();
           reduce_event(1, lrel);
           float r[8];
           load_vec(p.rbuf, r);
           layer_norm(r, W.ln2g, W.ln2b, xn2);
         } else if (dsc.type == ST_END) {
           release(sl);
+          qkv_complete();
+          attention_complete();
           stamp_layer(lrel, 3);
           reduce_event(p.parallel ? 0 : 2, lrel);
           break;
@@ -1089,6 +1168,7 @@ struct Consumer {
           // unexpected stage type: poison and stop
           fail_timeout(p.err, 99);
         }
+        if (slog) slog[2] = clock64();
       }
     }
     if (p.head_mode != HEAD_NONE) run_head();
@@ -1217,12 +1297,10 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
   const int pos = s.misc[0], step = s.misc[1];
 
   if (warp == p.ncw || (warp == p.ncw + 1 && p.pf_ahead > 0)) {
-    if ((tid & 31) == 0) {
-      Producer prod(p, s, warp != p.ncw);
-      prod.mlp_c0 = s.misc[3];
-      prod.mlp_c1 = s.misc[4];
-      prod.run(pos, step & 1, rank, cid);
-    }
+    Producer prod(p, s, tid & 31, warp != p.ncw);
+    prod.mlp_c0 = s.misc[3];
+    prod.mlp_c1 = s.misc[4];
+    prod.run(pos, step & 1, rank, cid);
   } else if (warp < p.ncw) {
     Consumer<DPL> c(p, s, tid, rank, cid, pos, step);
     c.run();

@@ -13,6 +13,15 @@ constexpr int kMaxBias = 512;
 // Upper bound on consumer warps (hidden <= 16 * 256 = 4096).
 constexpr int kMaxConsumerWarps = 16;
 
+// 8-row blocked layout of a [R][K] matrix (R % 8 == 0, K % 32 == 0): each
+// group of 8 consecutive rows is stored [K/32][8][32], so a group keeps the
+// byte range it has in row-major order and a warp-wide LDS.128 of one
+// 512-byte block is the B operand of two m16n8k16 MMAs.  Layout mode 2 of the
+// weight upload / synthesis paths (not used by the batch-1 kernel).
+__host__ __device__ inline size_t blk8_index(size_t r, size_t k, size_t K) {
+  return (r >> 3) * 8 * K + (k >> 5) * 256 + (r & 7) * 32 + (k & 31);
+}
+
 // Per-layer device pointers: the "layer descriptor table" built once per
 // context (graph mode re-uses it for every step).
 struct LayerW {
@@ -67,6 +76,7 @@ struct Params {
   int dyn_mlp;          // 1: MLP chunks grabbed dynamically (not bitwise reproducible)
   int head_weight_pct;  // static schedule: head-stage bytes weighted by this / 100
   int pf_ahead;         // L2 prefetcher lead over the ring producer (bytes); 0 = off
+  int mlp_gap;          // MLP pairs slotted after a head's QKV rows and after its KV share
   int debug;            // DBG_* bits (measurement only: results are garbage)
   // pointers
   const LayerW* layers;
@@ -87,14 +97,21 @@ struct Params {
   int trace_stride;
 };
 
-// Trace slots (per CTA): 0 producer ring-full wait ns, 1 consumer data wait ns
+// Trace slots (per CTA): 0 producer ring-full wait (SM cycles), 1 consumer data wait (cycles)
 // (thread 0), 2 kernel start, 3 consumer end, 4 head start, 5 head end,
 // then per layer l at 8 + 8*l: 0 layer start, 1 QKV exchanged, 2 context
 // ready, 3 END reached, 4 after grid barrier #1, 5 after grid barrier #2,
 // 6 first KV stage done, 7 attention state published, 8 partial stored
 // (before barrier #1), 9 fold done (before barrier #2).
-constexpr int kTraceHeader = 8;
+constexpr int kTraceHeader = 16;  // slots 8..15 spare
 constexpr int kTracePerLayer = 12;
+// Per-stage log of one layer (lrel = n_layers / 2) at the end of each CTA's
+// trace row: consumer thread 0 writes 4 words per stage (clock64 before wait,
+// after wait, after release; type | n << 8 | flags << 32), the producer 2 words
+// per push (before the empty-slot wait, after issue) from kTraceStageProd on.
+constexpr int kTraceStageMax = 64;
+constexpr int kTraceStageWords = 4 * kTraceStageMax + 2 * kTraceStageMax;
+constexpr int kTraceStageProd = 4 * kTraceStageMax;
 
 // Measurement-only modes (NFB_DEBUG env): stages arrive without data, or
 // consumers skip the arithmetic.  Used to split producer- vs consumer-bound time.

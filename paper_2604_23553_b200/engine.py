@@ -246,9 +246,10 @@ class Engine:
         check(self.lib.nfb_set_option(self._h, code, v), "nfb_set_option")
 
     def read_trace(self) -> np.ndarray:
-        """Per-CTA phase stamps of the last launch: [grid, 8 + 12*n_layers] (ns)."""
+        """Per-CTA phase stamps of the last launch: [grid, 16 + 12*n_layers + 384]
+        (ns; the last 384 words are the per-stage log of layer n_layers // 2)."""
         inf = self.info
-        stride = 8 + 12 * self.cfg.n_layers
+        stride = 16 + 12 * self.cfg.n_layers + 384
         out = np.zeros((inf["grid"], stride), np.uint64)
         check(self.lib.nfb_read_trace(self._h, out.ctypes.data_as(C.POINTER(C.c_ulonglong)), out.size),
               "nfb_read_trace")

@@ -24,10 +24,25 @@ __device__ __forceinline__ bool test_wait(uint64_t* b, uint32_t ph) {
                : "=r"(ok) : "r"(smem_u32(b)), "r"(ph) : "memory");
   return ok;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ int g_flag;
 template <int MODE>
 __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
   if (MODE == 0) { while (!try_wait(b, ph)) {} }
-  else { while (!test_wait(b, ph)) {} }
+  else if (MODE == 1) { while (!test_wait(b, ph)) {} }
+  else if (MODE == 2) {  // the decode kernel's pattern: globaltimer watchdog
+    if (try_wait(b, ph)) return;
+    const unsigned long long t0 = gtimer();
+    while (!try_wait(b, ph)) { if (gtimer() - t0 > 4000000000ull) g_flag = 1; }
+  } else {  // clock64 watchdog
+    if (try_wait(b, ph)) return;
+    const long long t0 = clock64();
+    while (!try_wait(b, ph)) { if (clock64() - t0 > 8000000000ll) g_flag = 1; }
+  }
 }
 
 template <int MODE>
@@ -70,15 +85,18 @@ int main() {
   long long* d; cudaMalloc(&d, 148 * 8);
   long long h[148];
   const int N = 20000;
-  for (int mode = 0; mode < 2; ++mode)
+  const char* names[] = {"try_wait ", "test_wait", "try+gtimer", "try+clock64"};
+  for (int mode = 0; mode < 4; ++mode)
     for (int ncw : {1, 4, 10}) {
       for (int rep = 0; rep < 2; ++rep) {
         if (mode == 0) ring<0><<<148, (ncw + 1) * 32>>>(N, 5, ncw, d);
-        else ring<1><<<148, (ncw + 1) * 32>>>(N, 5, ncw, d);
+        else if (mode == 1) ring<1><<<148, (ncw + 1) * 32>>>(N, 5, ncw, d);
+        else if (mode == 2) ring<2><<<148, (ncw + 1) * 32>>>(N, 5, ncw, d);
+        else ring<3><<<148, (ncw + 1) * 32>>>(N, 5, ncw, d);
         cudaDeviceSynchronize();
       }
       cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
-      printf("mode %s ncw %2d: %.1f cycles/stage\n", mode ? "test_wait" : "try_wait ", ncw, (double)h[0] / N);
+      printf("mode %s ncw %2d: %.1f cycles/stage\n", names[mode], ncw, (double)h[0] / N);
     }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -20,6 +20,9 @@ sys.path.insert(0, ROOT)
 from paper_2604_23553_b200 import Engine, mean_step_bytes, preset  # noqa: E402
 
 
+CYC = 1965.0  # SM clock64 ticks per us (accumulated waits are in cycles)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--preset", default="pythia-2.8b")
@@ -53,16 +56,17 @@ def main():
     C = info["cluster_size"]
     heads = np.array([(g // C) < cfg.n_heads for g in range(G)])
     out = {"info": info, "kernel_us": float(rel(tr[:, 3].max())),
-           "producer_wait_us_med": float(np.median(tr[:, 0]) / 1e3),
-           "consumer_wait_us_med": float(np.median(tr[:, 1]) / 1e3),
-           "consumer_wait_us_head_ctas": float(np.median(tr[heads, 1]) / 1e3),
-           "consumer_wait_us_mlp_ctas": float(np.median(tr[~heads, 1]) / 1e3),
-           "kv_stage_us_head_ctas": float(np.median(tr[heads, 6]) / 1e3),
-           "kv_wait_us_head_ctas": float(np.median(tr[heads, 7]) / 1e3),
+           "producer_wait_us_med": float(np.median(tr[:, 0]) / CYC),
+           "consumer_wait_us_med": float(np.median(tr[:, 1]) / CYC),
+           "consumer_wait_us_head_ctas": float(np.median(tr[heads, 1]) / CYC),
+           "consumer_wait_us_mlp_ctas": float(np.median(tr[~heads, 1]) / CYC),
+           "kv_stage_us_head_ctas": float(np.median(tr[heads, 6]) / CYC),
+           "kv_wait_us_head_ctas": float(np.median(tr[heads, 7]) / CYC),
+           "att_phase_us_cta0": [float(tr[0, 8 + k]) / CYC for k in range(4)],
            "head_phase_us": float(rel(tr[:, 5].max()) - rel(tr[:, 4].min())),
            "layers": []}
     for l in range(L):
-        b = 8 + 12 * l
+        b = 16 + 12 * l
         st, qkv, ctx, end, b1, b2, kv0, pub, pst, fld = (tr[:, b + k] for k in range(10))
         out["layers"].append({
             "start_us": float(rel(st.min())),
