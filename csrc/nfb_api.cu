@@ -197,6 +197,7 @@ struct nfb_ctx {
   int debug = 0;
   int pf_ahead = 0;  // L2 prefetcher lead (bytes); measured: no gain at C2
   int mlp_gap = 1;   // MLP pairs interleaved into the head schedule (split-phase cluster syncs)
+  int pair = 1;      // consumer stage pairing mask (1 MLP, 2 QKV, 4 W_out)
   unsigned long long* h_tok = nullptr;  // pinned [2]
   std::vector<void*> allocs;
 };
@@ -265,18 +266,20 @@ Params base_params(nfb_ctx* c) {
   p.head_weight_pct = c->head_weight_pct;
   p.pf_ahead = c->pf_ahead;
   p.mlp_gap = c->mlp_gap;
+  p.pair = c->pair;
   p.debug = c->debug;
   return p;
 }
 
 int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {
-  cudaError_t e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, st, c->coop);
+  const int variant = c->dpl + ((c->trace || c->debug) ? 2 : 0);
+  cudaError_t e = launch_decode(p, variant, c->grid, c->block, c->smem, st, c->coop);
   if (e != cudaSuccess && c->coop) {
     // Cooperative + cluster launch refused: fall back to the occupancy-checked
     // plain cluster launch (grid <= max active clusters, one CTA per SM).
     cudaGetLastError();
     c->coop = false;
-    e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, st, false);
+    e = launch_decode(p, variant, c->grid, c->block, c->smem, st, false);
   }
   if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
   return NFB_OK;
@@ -376,8 +379,8 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (max_seq < 1) return fail(NFB_EINVAL, "max_seq must be >= 1");
   int C = cluster_size > 0 ? cluster_size : 2;
   if (cluster_size <= 0 && getenv("NFB_CLUSTER")) C = atoi(getenv("NFB_CLUSTER"));
-  if (C > 8 || (3 * m.d_head) % C || m.d_head % C)
-    return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8 and divide d_head");
+  if (C > 8 || (3 * m.d_head) % C || m.d_head % C || ((3 * m.d_head) / C) % 4)
+    return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8, divide d_head and leave a multiple of 4 QKV rows per rank");
 
   nfb_ctx* c = new nfb_ctx();
   c->desc = m;
@@ -415,6 +418,8 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   c->smem = make_layout(probe).total;
 
   e = cudaFuncSetAttribute(decode_kernel_ptr(c->dpl), cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(decode_kernel_ptr(c->dpl + 2), cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem);
   if (e != cudaSuccess) return bail(fail(NFB_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e)));
   int nc = 0;
   e = max_active_clusters(c->dpl, C, c->block, c->smem, &nc);
@@ -427,6 +432,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (getenv("NFB_DEBUG")) c->debug = atoi(getenv("NFB_DEBUG"));
   if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
   if (getenv("NFB_MLP_GAP")) c->mlp_gap = atoi(getenv("NFB_MLP_GAP"));
+  if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
   c->n_clusters = nc;
   c->grid = nc * C;
 
@@ -858,8 +864,9 @@ int nfb_graph_capture(nfb_ctx* c) {
   // invalidate the capture).
   CK(cudaStreamSynchronize(c->stream));
   const Params p = decode_params(c);
+  const int variant = c->dpl + ((c->trace || c->debug) ? 2 : 0);
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  cudaError_t e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, c->stream, c->coop);
+  cudaError_t e = launch_decode(p, variant, c->grid, c->block, c->smem, c->stream, c->coop);
   cudaGraph_t g = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
   if ((e != cudaSuccess || e2 != cudaSuccess) && c->coop) {
@@ -867,7 +874,7 @@ int nfb_graph_capture(nfb_ctx* c) {
     cudaGetLastError();
     c->coop = false;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    e = launch_decode(p, c->dpl, c->grid, c->block, c->smem, c->stream, false);
+    e = launch_decode(p, variant, c->grid, c->block, c->smem, c->stream, false);
     e2 = cudaStreamEndCapture(c->stream, &g);
   }
   if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("capture launch: ") + cudaGetErrorString(e));

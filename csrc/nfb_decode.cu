@@ -41,6 +41,7 @@ enum StageType : int {
 constexpr int F_LAST = 1;   // last stage of a head's QKV / KV / W_out group
 constexpr int F_FIRST = 2;  // first stage of a row-dot batch (QKV / UP / LM)
 constexpr int F_FLUSH = 4;  // row-dot batch complete: reduce across warps now
+constexpr int F_PAIR = 8;   // the next stage is the same kind: consumers take both in one step
 
 struct Desc {
   int type;
@@ -60,15 +61,14 @@ struct Smem {
   float* ybuf;
   float* attst;
   float* ctx;
-  float* wst;
   float* wred;
   float* red_in;
   float* fold;
   float2* rope;   // (cos, sin) of this step's position, rd/2 entries
   float* ubias;   // up biases of this CTA's static MLP rows (kMaxBias)
+  LayerW* lw;     // [2] layer descriptors, by layer parity (prefetched a layer ahead)
   int* misc;
   int attst_stride;
-  int wst_stride;
 };
 
 __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, const Params& p) {
@@ -83,15 +83,14 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, cons
   s.ybuf = reinterpret_cast<float*>(base + L.ybuf);
   s.attst = reinterpret_cast<float*>(base + L.attst);
   s.ctx = reinterpret_cast<float*>(base + L.ctx);
-  s.wst = reinterpret_cast<float*>(base + L.wst);
   s.wred = reinterpret_cast<float*>(base + L.wred);
   s.red_in = reinterpret_cast<float*>(base + L.red_in);
   s.fold = reinterpret_cast<float*>(base + L.fold);
   s.rope = reinterpret_cast<float2*>(base + L.rope);
   s.misc = reinterpret_cast<int*>(base + L.misc);
   s.ubias = reinterpret_cast<float*>(base + L.ubias);
+  s.lw = reinterpret_cast<LayerW*>(base + L.lw);
   s.attst_stride = align_up(p.d + 2, 4);
-  s.wst_stride = align_up(p.d + 2, 4);
   return s;
 }
 
@@ -145,6 +144,7 @@ __device__ __forceinline__ void mlp_range_warp(const Params& p, int pos, uint32_
 // ===========================================================================
 // Producer
 // ===========================================================================
+template <bool TR>
 struct Producer {
   const Params& p;
   const Smem& s;
@@ -162,8 +162,10 @@ struct Producer {
   volatile uint32_t* shared_cum16;
 
   const int lane;
+  const uint32_t full_s, empty_s, ring_s;
   __device__ __forceinline__ Producer(const Params& p_, const Smem& s_, int lane_, bool prefetcher = false)
-      : p(p_), s(s_), pf(prefetcher), lane(lane_) {
+      : p(p_), s(s_), pf(prefetcher), lane(lane_), full_s(smem_u32(s_.full)), empty_s(smem_u32(s_.empty)),
+        ring_s(smem_u32(s_.ring)) {
     pol = policy_evict_first();
     shared_cum16 = reinterpret_cast<volatile uint32_t*>(s.misc + kMiscCum);
   }
@@ -187,9 +189,9 @@ struct Producer {
     const int slot = pslot;
     const uint32_t ph = pphase ^ 1u;
     unsigned long long* slog = nullptr;
-    if (p.trace) {
+    if (TR && p.trace != nullptr) {
       const unsigned long long t0 = clock64();
-      mbar_wait(&s.empty[slot], ph, p.err, 10);
+      mbar_wait_u32(empty_s + 8u * slot, ph, p.err, 10);
       wait_ns += clock64() - t0;
       if (log_on && n_log < kTraceStageMax) {
         if (lane == 0) {
@@ -200,18 +202,18 @@ struct Producer {
         ++n_log;
       }
     } else {
-      mbar_wait(&s.empty[slot], ph, p.err, 10);
+      mbar_wait_u32(empty_s + 8u * slot, ph, p.err, 10);
     }
     const uint32_t bytes = b0 + b1;
     if (lane == 0) {
       s.desc[slot] = Desc{type, a, n, flags};
-      unsigned char* dst = s.ring + (size_t)slot * p.slot_bytes;
-      if (bytes && !(p.debug & DBG_NO_COPY)) {
-        mbar_arrive_expect_tx(&s.full[slot], bytes);
-        bulk_g2s(dst, src0, b0, &s.full[slot], pol);
-        if (b1) bulk_g2s(dst + b0, src1, b1, &s.full[slot], pol);
+      const uint32_t dst = ring_s + (uint32_t)(slot * p.slot_bytes), fb = full_s + 8u * slot;
+      if (bytes && !((TR ? p.debug : 0) & DBG_NO_COPY)) {
+        mbar_arrive_expect_tx_u32(fb, bytes);
+        bulk_g2s_u32(dst, src0, b0, fb, pol);
+        if (b1) bulk_g2s_u32(dst + b0, src1, b1, fb, pol);
       } else {
-        mbar_arrive(&s.full[slot]);
+        mbar_arrive_u32(fb);
       }
       if (slog) slog[1] = clock64();
     }
@@ -248,14 +250,14 @@ struct Producer {
         next += 2;
       }
       const int ra = ca * p.stage_rows, na = min(p.stage_rows, p.m - ra);
-      push(ST_UP, ra, na, F_FIRST | (cb < 0 ? F_FLUSH : 0), W.wup + (size_t)ra * p.h, na * rowb);
+      push(ST_UP, ra, na, F_FIRST | (cb < 0 ? F_FLUSH : ((p.pair & 1) ? F_PAIR : 0)), W.wup + (size_t)ra * p.h, na * rowb);
       int rb = 0, nb = 0;
       if (cb >= 0) {
         rb = cb * p.stage_rows;
         nb = min(p.stage_rows, p.m - rb);
         push(ST_UP, rb, nb, F_FLUSH, W.wup + (size_t)rb * p.h, nb * rowb);
       }
-      push(ST_DOWN, ra, na, 0, W.wdT + (size_t)ra * p.h, na * rowb);
+      push(ST_DOWN, ra, na, (cb >= 0 && (p.pair & 1)) ? F_PAIR : 0, W.wdT + (size_t)ra * p.h, na * rowb);
       if (cb >= 0) push(ST_DOWN, rb, nb, na << 8, W.wdT + (size_t)rb * p.h, nb * rowb);
     }
   }
@@ -280,11 +282,13 @@ struct Producer {
         const int tag = hh << 8;
         // QKV rows of this head owned by this rank.
         const int q0 = (int)rank * p.rows_qkv;
-        for (int r = 0; r < p.rows_qkv; r += p.stage_rows) {
+        for (int r = 0, k = 0; r < p.rows_qkv; r += p.stage_rows, ++k) {
           const int n = min(p.stage_rows, p.rows_qkv - r);
           const int last = (r + n >= p.rows_qkv) ? F_LAST : 0;
           const int first = r == 0 ? F_FIRST : 0;
-          push(ST_QKV, q0 + r, n, tag | last | first, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h, n * rowb);
+          const int pair = ((p.pair & 2) && !(k & 1) && !last) ? F_PAIR : 0;
+          push(ST_QKV, q0 + r, n, tag | last | first | pair, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h,
+               n * rowb);
         }
         if (gap) emit_mlp(W, ctr, next, gap);
         // KV history share (partition_kv: first hist % C ranks get one extra).
@@ -302,10 +306,11 @@ struct Producer {
         if (gap) emit_mlp(W, ctr, next, gap);
         // W_out^T rows (context elements) owned by this rank.
         const int o0 = (int)rank * p.rows_o;
-        for (int r = 0; r < p.rows_o; r += p.stage_rows) {
+        for (int r = 0, k = 0; r < p.rows_o; r += p.stage_rows, ++k) {
           const int n = min(p.stage_rows, p.rows_o - r);
           const int last = (r + n >= p.rows_o) ? F_LAST : 0;
-          push(ST_WO, o0 + r, n, tag | last, W.woT + (size_t)(hh * d + o0 + r) * h, n * rowb);
+          const int pair = ((p.pair & 4) && !(k & 1) && !last) ? F_PAIR : 0;
+          push(ST_WO, o0 + r, n, tag | last | pair, W.woT + (size_t)(hh * d + o0 + r) * h, n * rowb);
         }
       }
       if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
@@ -329,7 +334,7 @@ struct Producer {
       }
       push(ST_HEAD_END, 0, 0, 0, nullptr, 0);
     }
-    if (p.trace && lane == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + 0] = wait_ns;
+    if ((TR && p.trace != nullptr) && lane == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + 0] = wait_ns;
   }
 };
 
@@ -412,6 +417,41 @@ __device__ __forceinline__ float butterfly8(float* v, int lane) {
   return v[0];
 }
 
+// 16-value reduce-scatter: afterwards lanes 2k, 2k+1 hold the warp sum of row
+// butterfly16_row(lane) = b4 * 8 + b3 * 4 + b2 * 2 + b1 (bits of the lane).
+__device__ __forceinline__ float butterfly16(float* v, int lane) {
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = b4 ? v[i] : v[i + 8];
+    const float keep = b4 ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b3 ? v[i] : v[i + 4];
+    const float keep = b3 ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? v[i] : v[i + 2];
+    const float keep = b2 ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const float send = b1 ? v[0] : v[1];
+    const float keep = b1 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+__device__ __forceinline__ int butterfly16_row(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
 __device__ __forceinline__ int butterfly_row(int lane) {
   return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
 }
@@ -455,7 +495,7 @@ __device__ __forceinline__ float consumer_sum(float v, float* scratch, int ncw, 
 // ===========================================================================
 // Consumer
 // ===========================================================================
-template <int DPL>
+template <int DPL, bool TR>
 struct Consumer {
   const Params& p;
   const Smem& s;
@@ -489,7 +529,9 @@ struct Consumer {
                       int pos_, int step_)
       : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(p_.ncw * 32),
         rank(rank_), cid(cid_), pos(pos_), step(step_), par(step_ & 1),
-        act(tid_ < (p_.h >> 3)), col(tid_ < (p_.h >> 3) ? tid_ : 0), rowb(p_.h * 2), ring_s(smem_u32(s_.ring)) {}
+        act(tid_ < (p_.h >> 3)), col(tid_ < (p_.h >> 3) ? tid_ : 0), rowb(p_.h * 2), ring_s(smem_u32(s_.ring)),
+        full_s(smem_u32(s_.full)), empty_s(smem_u32(s_.empty)), desc_s(smem_u32(s_.desc)) {}
+  const uint32_t full_s, empty_s, desc_s;  // shared-window addresses of the ring barriers / descriptors
 
   __device__ __forceinline__ void advance() {
     if (++slot == p.n_slots) {
@@ -501,25 +543,31 @@ struct Consumer {
   unsigned long long wait_ns = 0;
 
   __device__ __forceinline__ void stamp(int idx) {
-    if (p.trace && tid == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + idx] = globaltimer();
+    if ((TR && p.trace != nullptr) && tid == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + idx] = globaltimer();
   }
   __device__ __forceinline__ void stamp_layer(int lrel, int k) { stamp(kTraceHeader + kTracePerLayer * lrel + k); }
 
   unsigned long long last_wait = 0;
+  // trace-variant section timer: accumulates clock64 deltas of thread 0 into
+  // trace header slot k (8..15, zeroed at kernel start)
+  __device__ __forceinline__ long long tick() const { return (TR && p.trace != nullptr && tid == 0) ? clock64() : 0; }
+  __device__ __forceinline__ void tock(int k, long long t0) const {
+    if (TR && p.trace != nullptr && tid == 0) p.trace[(size_t)blockIdx.x * p.trace_stride + k] += clock64() - t0;
+  }
   __device__ __forceinline__ void wait_full(int sl, int code) {
-    if (p.trace && tid == 0) {
+    if ((TR && p.trace != nullptr) && tid == 0) {
       const unsigned long long t0 = clock64();
-      mbar_wait(&s.full[sl], phase, p.err, code);
+      mbar_wait_u32(full_s + 8u * sl, phase, p.err, code);
       last_wait = clock64() - t0;
       wait_ns += last_wait;
     } else {
-      mbar_wait(&s.full[sl], phase, p.err, code);
+      mbar_wait_u32(full_s + 8u * sl, phase, p.err, code);
     }
   }
 
   __device__ __forceinline__ void release(int sl) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&s.empty[sl]);
+    if (lane == 0) mbar_arrive_u32(empty_s + 8u * sl);
   }
 
   // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40)
@@ -591,6 +639,35 @@ struct Consumer {
     const float t = butterfly8(v, lane);
     const int row = butterfly_row(lane);
     if ((lane & 3) == 0 && row < n) wbase[row * p.ncw + warp] = t;
+  }
+
+  // Two stages (rows n0 of stage A then n1 of stage B) in one pass: 16
+  // independent row-dots, one 16-way reduce-scatter (butterfly16).
+  __device__ __forceinline__ void rowdot_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float2 (&x2)[4],
+                                              float* wbase) {
+    float v[2 * kRows];
+    {
+      uint4 w[kRows];
+      load_rows(sa, n0, w);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) v[r] = dot8x2(w[r], x2);
+    }
+    {
+      uint4 w[kRows];
+      load_rows(sb, n1, w);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) v[kRows + r] = dot8x2(w[r], x2);
+    }
+    const float t = butterfly16(v, lane);
+    const int row = butterfly16_row(lane);  // row of the pair (0..15); stage B rows start at 8
+    const int out = row < kRows ? row : n0 + row - kRows;
+    if (!(lane & 1) && (row < kRows ? row < n0 : row - kRows < n1)) wbase[out * p.ncw + warp] = t;
+  }
+
+  __device__ __forceinline__ void rowacc_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float (&ca)[kRows],
+                                              const float (&cb)[kRows]) {
+    rowacc_stage(sa, n0, ca);
+    rowacc_stage(sb, n1, cb);
   }
 
   __device__ __forceinline__ float row_total(const float* wrow) const {
@@ -793,7 +870,10 @@ struct Consumer {
       for (int i = 0; i < DPL; ++i) o2[i] = __shfl_sync(0xffffffffu, o[i], src);
       if (lane < T) merge_into(am, al, o, m2, l2, o2);
     }
-    float* ws = s.wst + warp * s.wst_stride;
+    // 2) the warp's state -> attst[rank][warp]; the whole rank block goes to
+    //    every peer in one bulk DSMEM copy (no intra-CTA merge pass)
+    const int blk = p.ncw * s.attst_stride;
+    float* ws = s.attst + ((int)rank * p.ncw + warp) * s.attst_stride;
     if (lane < T) {
 #pragma unroll
       for (int i = 0; i < DPL; ++i) ws[sub * DPL + i] = o[i];
@@ -802,36 +882,16 @@ struct Consumer {
         ws[d + 1] = al;
       }
     }
-    consumer_sync(nct);
-    // 2) CTA state, published to every rank's attst[rank]
-    float M = -INFINITY;
-    for (int w = 0; w < p.ncw; ++w) {
-      const float* wv = s.wst + w * s.wst_stride;
-      if (wv[d + 1] > 0.f) M = fmaxf(M, wv[d]);
-    }
-    float Lsum = 0.f;
-    for (int w = 0; w < p.ncw; ++w) {
-      const float* wv = s.wst + w * s.wst_stride;
-      if (wv[d + 1] > 0.f) Lsum += wv[d + 1] * fast_exp2(wv[d] - M);
-    }
-    const uint32_t my = smem_u32(s.attst + rank * s.attst_stride);
-    for (int t = tid; t < d + 2; t += nct) {
-      float val;
-      if (t < d) {
-        val = 0.f;
-        for (int w = 0; w < p.ncw; ++w) {
-          const float* wv = s.wst + w * s.wst_stride;
-          if (wv[d + 1] > 0.f) val += wv[t] * fast_exp2(wv[d] - M);
-        }
-      } else {
-        val = (t == d) ? M : Lsum;
-      }
-      for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(my + 4u * t, r), val);
-    }
+    fence_proxy_async_smem();
     consumer_sync(nct);
     stamp_layer(cur_layer - p.l0, 7);
-    if (tid == 0)
-      for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_att, r);
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)blk * 4u;
+      mbar_arrive_expect_tx_u32(smem_u32(s.bar_att), (uint32_t)(p.C - 1) * bytes);
+      const uint32_t src = smem_u32(s.attst + (int)rank * blk), bar = smem_u32(s.bar_att);
+      for (int r = 0; r < p.C; ++r)
+        if (r != (int)rank) bulk_s2cluster(mapa(src, r), src, bytes, mapa(bar, r));
+    }
     att_pending = true;
   }
 
@@ -841,28 +901,32 @@ struct Consumer {
     if (!att_pending) return;
     att_pending = false;
     const int d = p.d;
-    mbar_wait_cluster(s.bar_att, n_att & 1, p.err, 12);
+    long long t0 = tick();
+    mbar_wait_u32(smem_u32(s.bar_att), n_att & 1, p.err, 12);
+    tock(11, t0);
+    t0 = tick();
     ++n_att;
-    // 3) merge the C rank states in rank order -> context
+    // 3) merge the C * ncw (rank, warp) states in that fixed order -> context
+    const int ns = p.C * p.ncw;
     float Mc = -INFINITY;
-    for (int r = 0; r < p.C; ++r) {
-      const float* a = s.attst + r * s.attst_stride;
+    for (int k = 0; k < ns; ++k) {
+      const float* a = s.attst + k * s.attst_stride;
       if (a[d + 1] > 0.f) Mc = fmaxf(Mc, a[d]);
     }
-    float Lc = 0.f;
-    for (int r = 0; r < p.C; ++r) {
-      const float* a = s.attst + r * s.attst_stride;
-      if (a[d + 1] > 0.f) Lc += a[d + 1] * fast_exp2(a[d] - Mc);
-    }
     for (int t = tid; t < d; t += nct) {
-      float val = 0.f;
-      for (int r = 0; r < p.C; ++r) {
-        const float* a = s.attst + r * s.attst_stride;
-        if (a[d + 1] > 0.f) val += a[t] * fast_exp2(a[d] - Mc);
+      float val = 0.f, Lc = 0.f;
+      for (int k = 0; k < ns; ++k) {
+        const float* a = s.attst + k * s.attst_stride;
+        if (a[d + 1] > 0.f) {
+          const float f = fast_exp2(a[d] - Mc);
+          Lc += a[d + 1] * f;
+          val += a[t] * f;
+        }
       }
       s.ctx[t] = val / Lc;
     }
     consumer_sync(nct);
+    tock(12, t0);
     stamp_layer(cur_layer - p.l0, 2);
   }
 
@@ -870,9 +934,14 @@ struct Consumer {
   bool qkv_pending = false, att_pending = false;
   int pend_head = 0;
   __device__ __forceinline__ void qkv_publish(int head) {
-    consumer_sync(nct);  // all ybuf stores of this rank issued
-    if (tid == 0)
-      for (int r = 0; r < p.C; ++r) mbar_arrive_cluster(s.bar_qkv, r);
+    consumer_sync(nct);  // this rank's y rows are in its ybuf (and fenced)
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)p.rows_qkv * 4u;
+      mbar_arrive_expect_tx_u32(smem_u32(s.bar_qkv), (uint32_t)(p.C - 1) * bytes);
+      const uint32_t src = smem_u32(s.ybuf + (int)rank * p.rows_qkv), bar = smem_u32(s.bar_qkv);
+      for (int r = 0; r < p.C; ++r)
+        if (r != (int)rank) bulk_s2cluster(mapa(src, r), src, bytes, mapa(bar, r));
+    }
     qkv_pending = true;
     pend_head = head;
   }
@@ -882,12 +951,15 @@ struct Consumer {
     if (!qkv_pending) return;
     qkv_pending = false;
     const int head = pend_head;
-    mbar_wait_cluster(s.bar_qkv, n_qkv & 1, p.err, 11);
+    long long t0 = tick();
+    mbar_wait_u32(smem_u32(s.bar_qkv), n_qkv & 1, p.err, 11);
+    tock(8, t0);
+    t0 = tick();
     ++n_qkv;
     stamp_layer(cur_layer - p.l0, 1);
     // Rank 0 appends this step's rotated key and value to the cache (fp16).
     if (rank == 0) {
-      const LayerW& W = p.layers[cur_layer];
+      const LayerW& W = s.lw[(cur_layer - p.l0) & 1];
       const size_t off = ((size_t)head * p.max_seq + pos) * p.d;
       for (int j = tid; j < p.d; j += nct) {
         W.kc[off + j] = __float2half_rn(rope_at(s.ybuf + p.d, j));
@@ -895,6 +967,7 @@ struct Consumer {
       }
     }
     attention_begin();
+    tock(9, t0);
   }
 
   int cur_layer = 0;
@@ -906,15 +979,22 @@ struct Consumer {
     // 1) split-K partials of the cluster -> rank 0 via DSMEM
     if (p.C > 1) {
       if (rank != 0) {
+        // stage the partial in this CTA's own red_in slot, then one bulk copy
+        // into the same slot of rank 0 (complete_tx on rank 0's barrier)
+        float* stg = s.red_in + (size_t)(rank - 1) * h;
         if (act) {
-          const uint32_t dst = mapa(smem_u32(s.red_in + (size_t)(rank - 1) * h + tid * 8), 0);
-          st_cluster_v4(dst, acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y);
-          st_cluster_v4(dst + 16, acc2[2].x, acc2[2].y, acc2[3].x, acc2[3].y);
+          reinterpret_cast<float4*>(stg + tid * 8)[0] = make_float4(acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y);
+          reinterpret_cast<float4*>(stg + tid * 8)[1] = make_float4(acc2[2].x, acc2[2].y, acc2[3].x, acc2[3].y);
         }
+        fence_proxy_async_smem();
         consumer_sync(nct);
-        if (tid == 0) mbar_arrive_cluster(s.bar_red, 0);
+        if (tid == 0) {
+          const uint32_t src = smem_u32(stg);
+          bulk_s2cluster(mapa(src, 0), src, (uint32_t)h * 4u, mapa(smem_u32(s.bar_red), 0));
+        }
       } else {
-        mbar_wait_cluster(s.bar_red, n_red & 1, p.err, 13);
+        if (tid == 0) mbar_arrive_expect_tx_u32(smem_u32(s.bar_red), (uint32_t)((p.C - 1) * h * 4));
+        mbar_wait_u32(smem_u32(s.bar_red), n_red & 1, p.err, 13);
         if (act)
           for (int r = 1; r < p.C; ++r) {
             const float4 a = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8);
@@ -936,8 +1016,13 @@ struct Consumer {
     const int epc = (h + G - 1) / G;
     const int e0 = blockIdx.x * epc;
     const int nkg = max(1, nct / max(epc, 1));
-    const LayerW& W = p.layers[cur_layer];
+    const LayerW& W = s.lw[lrel & 1];
     const float* xin = p.xs + (size_t)lrel * h;
+    // descriptor of the next layer -> the other parity slot (its global-load
+    // latency hides under the grid barriers)
+    if (event != 1 && tid < (int)(sizeof(LayerW) / 8) && cur_layer + 1 < p.l1)
+      reinterpret_cast<unsigned long long*>(&s.lw[(lrel + 1) & 1])[tid] =
+          reinterpret_cast<const unsigned long long*>(&p.layers[cur_layer + 1])[tid];
     auto base_of = [&](int e) {
       if (event == 0) return __ldcg(xin + e) + __ldg(W.bo + e) + __ldg(W.bd + e);
       if (event == 1) return __ldcg(xin + e) + __ldg(W.bo + e);
@@ -1026,7 +1111,7 @@ struct Consumer {
     for (int l = p.l0; l < p.l1; ++l) {
       cur_layer = l;
       const int lrel = l - p.l0;
-      const LayerW& W = p.layers[l];
+      const LayerW& W = s.lw[lrel & 1];
       float x[8];
       if (l == p.l0 && p.in_mode == IN_TOKEN) {
         const int tok = s.misc[2];
@@ -1058,7 +1143,7 @@ struct Consumer {
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.f, 0.f);
 
-      const bool log_on = p.trace && tid == 0 && lrel == (p.l1 - p.l0) / 2;
+      const bool log_on = (TR && p.trace != nullptr) && tid == 0 && lrel == (p.l1 - p.l0) / 2;
       int n_log = 0;
       for (;;) {
         const int sl = slot;
@@ -1068,7 +1153,8 @@ struct Consumer {
           slog[0] = clock64();
         }
         wait_full(sl, 20);
-        const Desc dsc = s.desc[sl];
+        const uint4 dq = lds128_u32(desc_s + 16u * sl);
+        const Desc dsc{(int)dq.x, (int)dq.y, (int)dq.z, (int)dq.w};
         if (slog) {
           slog[1] = clock64();
           slog[3] = (unsigned long long)dsc.type | ((unsigned long long)dsc.n << 8) |
@@ -1078,35 +1164,54 @@ struct Consumer {
         const uint32_t sbuf = ring_s + (uint32_t)(sl * p.slot_bytes);
         advance();
         const int head = dsc.flags >> 8;
-        const bool last = dsc.flags & F_LAST;
+        bool last = dsc.flags & F_LAST;
+        // F_PAIR: the next ring stage is the same kind; take both in one step
+        const bool pair = dsc.flags & F_PAIR;
+        int sl2 = 0;
+        uint32_t sbuf2 = 0;
+        Desc dsc2{0, 0, 0, 0};
+        if (pair) {
+          sl2 = slot;
+          wait_full(sl2, 22);
+          const uint4 dq2 = lds128_u32(desc_s + 16u * sl2);
+          dsc2 = Desc{(int)dq2.x, (int)dq2.y, (int)dq2.z, (int)dq2.w};
+          sbuf2 = ring_s + (uint32_t)(sl2 * p.slot_bytes);
+          advance();
+          last = dsc2.flags & F_LAST;
+        }
         if (dsc.type == ST_QKV) {
           kv_first = true;
           if (dsc.flags & F_FIRST) {
             pend = 0;
             qbias = tid < p.rows_qkv ? __ldg(W.bqkv + head * 3 * p.d + (int)rank * p.rows_qkv + tid) : 0.f;
           }
-          if (!(p.debug & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
+            if (pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn1, s.wred + pend * p.ncw);
+            else rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
+          }
           release(sl);
-          pend += dsc.n;
+          if (pair) release(sl2);
+          pend += dsc.n + dsc2.n;
           if (last) {
             // all of this rank's QKV rows: one cross-warp combine, then
             // publish y into every cluster rank's ybuf through DSMEM
+            const long long tq = tick();
             consumer_sync(nct);
             const int q0 = (int)rank * p.rows_qkv;
             for (int t = tid; t < p.rows_qkv; t += nct) {
               const float b = t < nct ? qbias : __ldg(W.bqkv + head * 3 * p.d + q0 + t);
-              const float y = row_total(s.wred + t * p.ncw) + b;
-              const uint32_t a = smem_u32(s.ybuf + q0 + t);
-              for (int r = 0; r < p.C; ++r) st_cluster_f32(mapa(a, r), y);
+              s.ybuf[q0 + t] = row_total(s.wred + t * p.ncw) + b;
             }
+            fence_proxy_async_smem();
             qkv_publish(head);
+            tock(13, tq);
           }
         } else if (dsc.type == ST_KV) {
           qkv_complete();
-          const unsigned long long ta = (p.trace && tid == 0) ? clock64() : 0ull;
-          if (!(p.debug & DBG_NO_COMPUTE)) attention_stage(buf, dsc.n);
+          const unsigned long long ta = ((TR && p.trace != nullptr) && tid == 0) ? clock64() : 0ull;
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) attention_stage(buf, dsc.n);
           release(sl);
-          if (p.trace && tid == 0) {
+          if ((TR && p.trace != nullptr) && tid == 0) {
             kv_ns += clock64() - ta;
             kvwait_ns += last_wait;
           }
@@ -1115,24 +1220,38 @@ struct Consumer {
             kv_first = false;
           }
           if (last) {
+            const long long t0 = tick();
             if ((int)rank == p.C - 1) attention_new_token();
             attention_publish();
+            tock(10, t0);
           }
         } else if (dsc.type == ST_WO) {
           attention_complete();
-          float c[kRows];
+          float c[kRows], c2[kRows];
 #pragma unroll
-          for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? s.ctx[dsc.a + r] : 0.f;
-          if (!(p.debug & DBG_NO_COMPUTE)) rowacc_stage(sbuf, dsc.n, c);
+          for (int r = 0; r < kRows; ++r) {
+            c[r] = r < dsc.n ? s.ctx[dsc.a + r] : 0.f;
+            c2[r] = r < dsc2.n ? s.ctx[dsc2.a + r] : 0.f;
+          }
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
+            if (pair) rowacc_pair(sbuf, dsc.n, sbuf2, dsc2.n, c, c2);
+            else rowacc_stage(sbuf, dsc.n, c);
+          }
           release(sl);
+          if (pair) release(sl2);
         } else if (dsc.type == ST_UP) {
           if (dsc.flags & F_FIRST) pend = 0;
           if (lane >= pend && lane < pend + dsc.n) grow = dsc.a + lane - pend;
+          if (pair && lane >= pend + dsc.n && lane < pend + dsc.n + dsc2.n) grow = dsc2.a + lane - pend - dsc.n;
           float* wb = s.wred + (gbuf * 2 * kRows + pend) * p.ncw;
-          if (!(p.debug & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn2, wb);
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
+            if (pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn2, wb);
+            else rowdot_stage(sbuf, dsc.n, xn2, wb);
+          }
           release(sl);
-          pend += dsc.n;
-          if (dsc.flags & F_FLUSH) {
+          if (pair) release(sl2);
+          pend += dsc.n + dsc2.n;
+          if ((dsc.flags | dsc2.flags) & F_FLUSH) {
             consumer_sync(nct);
             const float* wr = s.wred + (gbuf * 2 * kRows + lane) * p.ncw;
             const int bi = grow - ub0;
@@ -1141,14 +1260,24 @@ struct Consumer {
             gbuf ^= 1;
           }
         } else if (dsc.type == ST_DOWN) {
-          const int off = dsc.flags >> 8;
-          float c[kRows];
+          const int off = dsc.flags >> 8, off2 = dsc2.flags >> 8;
+          float c[kRows], c2[kRows];
 #pragma unroll
-          for (int r = 0; r < kRows; ++r) c[r] = __shfl_sync(0xffffffffu, gval, (off + r) & 31);
+          for (int r = 0; r < kRows; ++r) {
+            c[r] = __shfl_sync(0xffffffffu, gval, (off + r) & 31);
+            c2[r] = __shfl_sync(0xffffffffu, gval, (off2 + r) & 31);
+          }
 #pragma unroll
-          for (int r = 0; r < kRows; ++r) c[r] = r < dsc.n ? c[r] : 0.f;
-          if (!(p.debug & DBG_NO_COMPUTE)) rowacc_stage(sbuf, dsc.n, c);
+          for (int r = 0; r < kRows; ++r) {
+            c[r] = r < dsc.n ? c[r] : 0.f;
+            c2[r] = r < dsc2.n ? c2[r] : 0.f;
+          }
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
+            if (pair) rowacc_pair(sbuf, dsc.n, sbuf2, dsc2.n, c, c2);
+            else rowacc_stage(sbuf, dsc.n, c);
+          }
           release(sl);
+          if (pair) release(sl2);
         } else if (dsc.type == ST_SYNC) {
           release(sl);
           qkv_complete();
@@ -1173,7 +1302,7 @@ struct Consumer {
     }
     if (p.head_mode != HEAD_NONE) run_head();
     stamp(3);
-    if (p.trace && tid == 0) {
+    if ((TR && p.trace != nullptr) && tid == 0) {
       p.trace[(size_t)blockIdx.x * p.trace_stride + 1] = wait_ns;
       p.trace[(size_t)blockIdx.x * p.trace_stride + 6] = kv_ns;
       p.trace[(size_t)blockIdx.x * p.trace_stride + 7] = kvwait_ns;
@@ -1206,7 +1335,7 @@ struct Consumer {
         } else {
           lm_a1 = dsc.a;
         }
-        if (!(p.debug & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * p.ncw);
+        if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * p.ncw);
         release(sl);
         pend += dsc.n;
         if (dsc.flags & F_FLUSH) {
@@ -1241,7 +1370,7 @@ struct Consumer {
 // ===========================================================================
 // Kernel
 // ===========================================================================
-template <int DPL, int MAXT>
+template <int DPL, int MAXT, bool TR>
 __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Layout L = make_layout(p);
@@ -1255,9 +1384,11 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], p.ncw);
     }
-    mbar_init(s.bar_qkv, p.C);
-    mbar_init(s.bar_att, p.C);
-    mbar_init(s.bar_red, p.C > 1 ? p.C - 1 : 1);
+    // cluster exchange barriers: one local arrive (with expect_tx) per phase;
+    // the peers' bulk DSMEM copies complete the transaction bytes
+    mbar_init(s.bar_qkv, 1);
+    mbar_init(s.bar_att, 1);
+    mbar_init(s.bar_red, 1);
     fence_mbar_init();
     const int pos = *reinterpret_cast<volatile int*>(p.state);
     const int step = *reinterpret_cast<volatile int*>(p.state + 1);
@@ -1272,6 +1403,8 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
     }
     s.misc[2] = tok;
     s.misc[kMiscCum] = 0;
+    if (TR && p.trace != nullptr)
+      for (int k = 8; k < 16; ++k) p.trace[(size_t)blockIdx.x * p.trace_stride + k] = 0;
     if (blockIdx.x == 0) {
       // Slots of the other parity are idle during this launch: reset them.
       for (int i = 0; i < p.ctr_stride; ++i) p.ctr[(par ^ 1) * p.ctr_stride + i] = 0;
@@ -1279,6 +1412,8 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
       if (p.in_mode == IN_TOKEN && step < p.max_seq) p.tokens[step] = tok;
     }
   }
+  if (tid < (int)(sizeof(LayerW) / 8))
+    reinterpret_cast<unsigned long long*>(&s.lw[0])[tid] = reinterpret_cast<const unsigned long long*>(&p.layers[p.l0])[tid];
   __syncthreads();
   {
     const int half = p.rd >> 1;
@@ -1297,21 +1432,23 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
   const int pos = s.misc[0], step = s.misc[1];
 
   if (warp == p.ncw || (warp == p.ncw + 1 && p.pf_ahead > 0)) {
-    Producer prod(p, s, tid & 31, warp != p.ncw);
+    Producer<TR> prod(p, s, tid & 31, warp != p.ncw);
     prod.mlp_c0 = s.misc[3];
     prod.mlp_c1 = s.misc[4];
     prod.run(pos, step & 1, rank, cid);
   } else if (warp < p.ncw) {
-    Consumer<DPL> c(p, s, tid, rank, cid, pos, step);
+    Consumer<DPL, TR> c(p, s, tid, rank, cid, pos, step);
     c.run();
   }
   cluster_sync_all();
 }
 
-// Explicit instantiations used by the host launcher: 8 head dims per lane,
-// block of <= 12 warps (hidden <= 2560) or <= 18 warps (hidden <= 4096).
-template __global__ void decode_kernel<8, 384>(const Params);
-template __global__ void decode_kernel<8, 576>(const Params);
+// Kernel variants: block <= 384 threads (hidden <= 2560) or <= 576 (hidden
+// <= 4096), each without / with the trace + measurement-debug paths compiled
+// in (variant = size + 2 * trace).
+#define NFB_VARIANTS(X) X(0, 384, false) X(1, 576, false) X(2, 384, true) X(3, 576, true)
+#define NFB_INST(i, t, tr) template __global__ void decode_kernel<8, t, tr>(const Params);
+NFB_VARIANTS(NFB_INST)
 
 }  // namespace nfb
 
@@ -1320,13 +1457,15 @@ template __global__ void decode_kernel<8, 576>(const Params);
 // ===========================================================================
 namespace nfb {
 
-// `variant`: 0 -> block <= 384 threads, 1 -> block <= 576 threads.
 const void* decode_kernel_ptr(int variant) {
-  return variant == 0 ? reinterpret_cast<const void*>(&decode_kernel<8, 384>)
-                      : reinterpret_cast<const void*>(&decode_kernel<8, 576>);
+#define NFB_PTR(i, t, tr) \
+  if (variant == i) return reinterpret_cast<const void*>(&decode_kernel<8, t, tr>);
+  NFB_VARIANTS(NFB_PTR)
+#undef NFB_PTR
+  return nullptr;
 }
 
-cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
+cudaError_t launch_decode(const Params& p, int variant, int grid, int block, int smem, cudaStream_t st,
                           bool cooperative) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -1346,8 +1485,11 @@ cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int sme
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  if (dpl == 0) return cudaLaunchKernelEx(&cfg, decode_kernel<8, 384>, p);
-  return cudaLaunchKernelEx(&cfg, decode_kernel<8, 576>, p);
+#define NFB_LAUNCH(i, t, tr) \
+  if (variant == i) return cudaLaunchKernelEx(&cfg, decode_kernel<8, t, tr>, p);
+  NFB_VARIANTS(NFB_LAUNCH)
+#undef NFB_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out) {

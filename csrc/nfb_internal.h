@@ -77,6 +77,7 @@ struct Params {
   int head_weight_pct;  // static schedule: head-stage bytes weighted by this / 100
   int pf_ahead;         // L2 prefetcher lead over the ring producer (bytes); 0 = off
   int mlp_gap;          // MLP pairs slotted after a head's QKV rows and after its KV share
+  int pair;             // stage pairing (consumers take 2 ring stages per step): 1 MLP, 2 QKV, 4 W_out
   int debug;            // DBG_* bits (measurement only: results are garbage)
   // pointers
   const LayerW* layers;
@@ -124,7 +125,7 @@ constexpr int kMiscCum = 56;
 
 // Shared-memory carve-up, computed identically on host and device.
 struct Layout {
-  int ring, full, empty, desc, bars, ybuf, attst, ctx, wst, wred, red_in, fold, rope, misc, ubias, total;
+  int ring, full, empty, desc, bars, ybuf, attst, ctx, wred, red_in, fold, rope, misc, ubias, lw, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -139,15 +140,15 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.desc = o;   o += 16 * p.n_slots;
   L.bars = o;   o += 8 * 4;
   L.ybuf = o;   o += 4 * align_up(3 * p.d, 4);
-  L.attst = o;  o += 4 * p.C * align_up(p.d + 2, 4);
+  L.attst = o;  o += 4 * p.C * p.ncw * align_up(p.d + 2, 4);  // [rank][warp] softmax states
   L.ctx = o;    o += 4 * align_up(p.d, 4);
-  L.wst = o;    o += 4 * p.ncw * align_up(p.d + 2, 4);
   L.wred = o;   o += 4 * p.ncw * (align_up(p.rows_qkv, 8) > 4 * kRows ? align_up(p.rows_qkv, 8) : 4 * kRows);
   L.red_in = o; o += 4 * (p.C - 1) * p.h;
   L.fold = o;   o += 4 * 32 * p.ncw;
   L.rope = o;   o += 4 * align_up(p.rd, 4);
   L.misc = o;   o += 4 * 64;
   L.ubias = o;  o += 4 * kMaxBias;
+  L.lw = o;     o += 2 * (int)sizeof(LayerW);
   L.total = align_up(o, 128);
   return L;
 }
