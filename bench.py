@@ -46,7 +46,18 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    return ap.parse_args()
+    ap.add_argument("--model", default="pythia-2.8b",
+                    help="pythia-2.8b (BASELINE configs[1], the headline) or pythia-6.9b (configs[2])")
+    ap.add_argument("--context", type=int, default=0, help="KV prefix length (default 1024 / 2048)")
+    a = ap.parse_args()
+    global CONTEXT, WORKLOAD
+    if not a.context:
+        a.context = 2048 if a.model == "pythia-6.9b" else 1024
+    CONTEXT = a.context
+    if a.model != "pythia-2.8b" or CONTEXT != 1024:
+        name = {"pythia-2.8b": "Pythia-2.8B", "pythia-6.9b": "Pythia-6.9B"}.get(a.model, a.model)
+        WORKLOAD = f"{name} random-init, bs=1, ctx {CONTEXT}, greedy decode, CUDA graph, 1 launch/token"
+    return a
 
 
 def dist_setup():
@@ -133,7 +144,7 @@ def cpu_reference(seconds: float, tokens_cap: int | None = None):
     change the timing).  Returns (tokens_per_s, sample description, threads)."""
     from oracle import neox_oracle as O
     from paper_2604_23553_b200 import preset
-    cfg = preset("pythia-2.8b")
+    cfg = preset(MODEL)
     s = O.Shape.of(cfg)
     rng = np.random.default_rng(0)
     p = {}
@@ -171,7 +182,7 @@ def cpu_reference(seconds: float, tokens_cap: int | None = None):
             break
     per = statistics.mean(t_tok)
     sample = (f"{done} decode token(s) of the float64 numpy port of decoder_block_golden "
-              f"(oracle/neox_oracle.block_step) x32 Pythia-2.8B layers (shared layer weights) + "
+              f"(oracle/neox_oracle.block_step) x{s.n_layers} {MODEL} layers (shared layer weights) + "
               f"final LN + LM-head GEMV + argmax, ctx {CONTEXT}, {threads} BLAS threads")
     return 1.0 / per, sample, threads, done
 
@@ -206,7 +217,7 @@ def run_ours(args, world, rank, local):
     import torch
     from paper_2604_23553_b200 import Engine, mean_step_bytes, preset
     torch.cuda.set_device(local)
-    cfg = preset("pythia-2.8b")
+    cfg = preset(MODEL)
     K, W = args.steps, max(args.warmup, 3)
     max_seq = CONTEXT + max(K, W) + 8
     eng = Engine(cfg, max_seq=max_seq, device=local)
@@ -266,8 +277,8 @@ def run_ours(args, world, rank, local):
     achieved = bytes_step / (t / K) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
+    if os.path.exists(tp) and MODEL == "pythia-2.8b" and CONTEXT == 1024:
+        with open(tp) as f:  # ncu capture of the headline workload only
             traffic = json.load(f).get("dram_bytes_per_launch")
     line = {
         "metric": METRIC,
@@ -285,7 +296,7 @@ def run_ours(args, world, rank, local):
         "data": "synthetic (random-init SplitMix64 weights, synthetic KV prefix)",
         "config": {"workload": WORKLOAD, "context": CONTEXT, "batch": 1, "decode_steps": K,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "no flush: 5.65 GB/step working set >> 126 MB L2"},
+                   "l2": f"no flush: {mean_step_bytes(cfg, CONTEXT, K) / 1e9:.2f} GB/step working set >> 126 MB L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
                      "bytes_per_launch": bytes_step, "peak_kind": kind},
@@ -302,8 +313,13 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+MODEL = "pythia-2.8b"
+
+
 def main():
+    global MODEL
     args = parse()
+    MODEL = args.model
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))

@@ -402,10 +402,13 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
 
-  c->ncw = (m.hidden / 8 + 31) / 32;
+  // consumer thread t owns 16-byte hidden chunks t (+ nct for 2 chunks/thread)
+  const int nch = m.hidden / 8 > 320 ? 2 : 1;
+  c->ncw = (m.hidden / 8 / nch + 31) / 32;
   c->block = (c->ncw + 2) * 32;  // consumers + ring producer warp + L2 prefetcher warp
-  c->dpl = c->block <= 384 ? 0 : 1;  // kernel variant (max threads per block)
-  c->stage_rows = m.hidden >= 4096 ? 4 : kRows;
+  c->dpl = nch - 1;              // kernel variant (chunks per consumer thread)
+  c->stage_rows = kRows;  // 8-row stages (64 KB at hidden 4096: 3 ring slots)
+  if (getenv("NFB_STAGE_ROWS")) c->stage_rows = std::max(1, std::min(kRows, atoi(getenv("NFB_STAGE_ROWS"))));
   c->slot_bytes = std::max(c->stage_rows * m.hidden * 2, 4 * m.d_head * 2 * 2);
   c->kv_pos = c->slot_bytes / (4 * m.d_head);
   Params probe = base_params(c);

@@ -495,15 +495,18 @@ __device__ __forceinline__ float consumer_sum(float v, float* scratch, int ncw, 
 // ===========================================================================
 // Consumer
 // ===========================================================================
-template <int DPL, bool TR>
+// NCH: 16-byte hidden chunks owned per consumer thread (chunk k of thread t is
+// t + k * nct): 1 for hidden <= 2560, 2 for wider models (hidden 4096 with 8
+// consumer warps, so every variant keeps the 384-thread register budget).
+template <int DPL, bool TR, int NCH>
 struct Consumer {
   const Params& p;
   const Smem& s;
   const int tid, warp, lane, nct;
   const uint32_t rank, cid;
   const int pos, step, par;
-  const bool act;   // owns a live hidden chunk
-  const int col;    // 16-byte column this thread reads from a weight row (0 if !act)
+  bool act[NCH];    // chunk k is a live hidden chunk
+  int col[NCH];     // 16-byte column of chunk k in a weight row (0 if !act[k])
   const int rowb;   // bytes per weight row (hidden * 2)
   const uint32_t ring_s;  // shared-window address of the stage ring
   bool kv_first = false;
@@ -518,7 +521,7 @@ struct Consumer {
   uint32_t phase = 0;
   int n_qkv = 0, n_att = 0, n_red = 0, n_events = 0;
   // registers
-  float2 xn1[4], xn2[4], acc2[4];  // LN1(x), LN2(x), split-K accumulator (8 hidden elems)
+  float2 xn1[NCH][4], xn2[NCH][4], acc2[NCH][4];  // LN1(x), LN2(x), split-K accumulator per chunk
   float gval = 0.f;                      // gelu(up) for row `lane` of the last UP stage
   // attention state (valid lanes of a position group)
   float qr[DPL], o[DPL], am, al;
@@ -529,8 +532,15 @@ struct Consumer {
                       int pos_, int step_)
       : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(p_.ncw * 32),
         rank(rank_), cid(cid_), pos(pos_), step(step_), par(step_ & 1),
-        act(tid_ < (p_.h >> 3)), col(tid_ < (p_.h >> 3) ? tid_ : 0), rowb(p_.h * 2), ring_s(smem_u32(s_.ring)),
-        full_s(smem_u32(s_.full)), empty_s(smem_u32(s_.empty)), desc_s(smem_u32(s_.desc)) {}
+        rowb(p_.h * 2), ring_s(smem_u32(s_.ring)),
+        full_s(smem_u32(s_.full)), empty_s(smem_u32(s_.empty)), desc_s(smem_u32(s_.desc)) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int c = tid_ + k * p_.ncw * 32;
+      act[k] = c < (p_.h >> 3);
+      col[k] = act[k] ? c : 0;
+    }
+  }
   const uint32_t full_s, empty_s, desc_s;  // shared-window addresses of the ring barriers / descriptors
 
   __device__ __forceinline__ void advance() {
@@ -571,44 +581,55 @@ struct Consumer {
   }
 
   // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40)
-  __device__ __forceinline__ void layer_norm(const float* x, const float* g, const float* b, float2 (&out)[4]) {
+  __device__ __forceinline__ void layer_norm(const float (&x)[NCH][8], const float* g, const float* b,
+                                             float2 (&out)[NCH][4]) {
     float sm = 0.f;
-    if (act)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) sm += x[i];
+    for (int k = 0; k < NCH; ++k)
+      if (act[k])
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm += x[k][i];
     const float mu = consumer_sum(sm, reinterpret_cast<float*>(s.misc) + 16, p.ncw, warp, lane) / p.h;
     float sq = 0.f;
-    if (act)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) sq += (x[i] - mu) * (x[i] - mu);
+    for (int k = 0; k < NCH; ++k)
+      if (act[k])
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sq += (x[k][i] - mu) * (x[k][i] - mu);
     const float var = consumer_sum(sq, reinterpret_cast<float*>(s.misc) + 32, p.ncw, warp, lane) / p.h;
     const float rstd = rsqrtf(var + p.eps);
-    if (act) {
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(g) + 2 * tid);
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(g) + 2 * tid + 1);
-      const float4 b0 = __ldg(reinterpret_cast<const float4*>(b) + 2 * tid);
-      const float4 b1 = __ldg(reinterpret_cast<const float4*>(b) + 2 * tid + 1);
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        out[i] = make_float2((x[2 * i] - mu) * rstd * gg[2 * i] + bb[2 * i],
-                             (x[2 * i + 1] - mu) * rstd * gg[2 * i + 1] + bb[2 * i + 1]);
-    } else {
+    for (int k = 0; k < NCH; ++k) {
+      if (act[k]) {
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(g) + 2 * col[k]);
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(g) + 2 * col[k] + 1);
+        const float4 b0 = __ldg(reinterpret_cast<const float4*>(b) + 2 * col[k]);
+        const float4 b1 = __ldg(reinterpret_cast<const float4*>(b) + 2 * col[k] + 1);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) out[i] = make_float2(0.f, 0.f);
+        for (int i = 0; i < 4; ++i)
+          out[k][i] = make_float2((x[k][2 * i] - mu) * rstd * gg[2 * i] + bb[2 * i],
+                                  (x[k][2 * i + 1] - mu) * rstd * gg[2 * i + 1] + bb[2 * i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) out[k][i] = make_float2(0.f, 0.f);
+      }
     }
   }
 
-  __device__ __forceinline__ void load_vec(const float* src, float* x) {
-    if (act) {
-      const float4 a = __ldcg(reinterpret_cast<const float4*>(src) + 2 * tid);
-      const float4 b = __ldcg(reinterpret_cast<const float4*>(src) + 2 * tid + 1);
-      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-      x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-    } else {
+  __device__ __forceinline__ void load_vec(const float* src, float (&x)[NCH][8]) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    for (int k = 0; k < NCH; ++k) {
+      if (act[k]) {
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(src) + 2 * col[k]);
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(src) + 2 * col[k] + 1);
+        x[k][0] = a.x; x[k][1] = a.y; x[k][2] = a.z; x[k][3] = a.w;
+        x[k][4] = b.x; x[k][5] = b.y; x[k][6] = b.z; x[k][7] = b.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[k][i] = 0.f;
+      }
     }
   }
 
@@ -616,8 +637,8 @@ struct Consumer {
   // (rows >= n read as zero; inactive threads read column 0 and are masked by
   // zero inputs / never store their accumulators).  Addresses are 32-bit
   // shared-window offsets (ld.shared), so no generic->shared conversion.
-  __device__ __forceinline__ void load_rows(uint32_t sl, int n, uint4 (&w)[kRows]) const {
-    const uint32_t b = sl + (uint32_t)col * 16u;
+  __device__ __forceinline__ void load_rows(uint32_t sl, int n, int colk, uint4 (&w)[kRows]) const {
+    const uint32_t b = sl + (uint32_t)colk * 16u;
     if (n == kRows) {
 #pragma unroll
       for (int r = 0; r < kRows; ++r) w[r] = lds128(b + (uint32_t)(r * rowb));
@@ -630,12 +651,15 @@ struct Consumer {
   // Row-dot of the stage's rows with `xv`: the warp sum of row r lands in
   // wbase[r * ncw + warp] (combine across warps with row_total after a
   // consumer barrier).
-  __device__ __forceinline__ void rowdot_stage(uint32_t sl, int n, const float2 (&x2)[4], float* wbase) {
-    uint4 w[kRows];
-    load_rows(sl, n, w);
+  __device__ __forceinline__ void rowdot_stage(uint32_t sl, int n, const float2 (&x2)[NCH][4], float* wbase) {
     float v[kRows];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) v[r] = dot8x2(w[r], x2);
+    for (int k = 0; k < NCH; ++k) {
+      uint4 w[kRows];
+      load_rows(sl, n, col[k], w);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) v[r] = k ? v[r] + dot8x2(w[r], x2[k]) : dot8x2(w[r], x2[k]);
+    }
     const float t = butterfly8(v, lane);
     const int row = butterfly_row(lane);
     if ((lane & 3) == 0 && row < n) wbase[row * p.ncw + warp] = t;
@@ -643,20 +667,23 @@ struct Consumer {
 
   // Two stages (rows n0 of stage A then n1 of stage B) in one pass: 16
   // independent row-dots, one 16-way reduce-scatter (butterfly16).
-  __device__ __forceinline__ void rowdot_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float2 (&x2)[4],
+  __device__ __forceinline__ void rowdot_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float2 (&x2)[NCH][4],
                                               float* wbase) {
     float v[2 * kRows];
-    {
-      uint4 w[kRows];
-      load_rows(sa, n0, w);
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) v[r] = dot8x2(w[r], x2);
+    for (int k = 0; k < NCH; ++k) {
+      uint4 w[kRows];
+      load_rows(sa, n0, col[k], w);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) v[r] = k ? v[r] + dot8x2(w[r], x2[k]) : dot8x2(w[r], x2[k]);
     }
-    {
-      uint4 w[kRows];
-      load_rows(sb, n1, w);
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) v[kRows + r] = dot8x2(w[r], x2);
+    for (int k = 0; k < NCH; ++k) {
+      uint4 w[kRows];
+      load_rows(sb, n1, col[k], w);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+        v[kRows + r] = k ? v[kRows + r] + dot8x2(w[r], x2[k]) : dot8x2(w[r], x2[k]);
     }
     const float t = butterfly16(v, lane);
     const int row = butterfly16_row(lane);  // row of the pair (0..15); stage B rows start at 8
@@ -683,14 +710,17 @@ struct Consumer {
   // acc += coef[r] * row r over the stage's rows (transposed projections);
   // coef[r] must be 0 for r >= n.
   __device__ __forceinline__ void rowacc_stage(uint32_t sl, int n, const float (&coef)[kRows]) {
-    uint4 w[kRows];
-    load_rows(sl, n, w);
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const __half2* hp = reinterpret_cast<const __half2*>(&w[r]);
-      const float2 c2 = make_float2(coef[r], coef[r]);
+    for (int k = 0; k < NCH; ++k) {
+      uint4 w[kRows];
+      load_rows(sl, n, col[k], w);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc2[i] = ffma2(c2, __half22float2(hp[i]), acc2[i]);
+      for (int r = 0; r < kRows; ++r) {
+        const __half2* hp = reinterpret_cast<const __half2*>(&w[r]);
+        const float2 c2 = make_float2(coef[r], coef[r]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc2[k][i] = ffma2(c2, __half22float2(hp[i]), acc2[k][i]);
+      }
     }
   }
 
@@ -982,10 +1012,13 @@ struct Consumer {
         // stage the partial in this CTA's own red_in slot, then one bulk copy
         // into the same slot of rank 0 (complete_tx on rank 0's barrier)
         float* stg = s.red_in + (size_t)(rank - 1) * h;
-        if (act) {
-          reinterpret_cast<float4*>(stg + tid * 8)[0] = make_float4(acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y);
-          reinterpret_cast<float4*>(stg + tid * 8)[1] = make_float4(acc2[2].x, acc2[2].y, acc2[3].x, acc2[3].y);
-        }
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          if (act[k]) {
+            float4* q = reinterpret_cast<float4*>(stg + col[k] * 8);
+            q[0] = make_float4(acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y);
+            q[1] = make_float4(acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y);
+          }
         fence_proxy_async_smem();
         consumer_sync(nct);
         if (tid == 0) {
@@ -995,21 +1028,27 @@ struct Consumer {
       } else {
         if (tid == 0) mbar_arrive_expect_tx_u32(smem_u32(s.bar_red), (uint32_t)((p.C - 1) * h * 4));
         mbar_wait_u32(smem_u32(s.bar_red), n_red & 1, p.err, 13);
-        if (act)
-          for (int r = 1; r < p.C; ++r) {
-            const float4 a = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8);
-            const float4 b = *reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + tid * 8 + 4);
-            acc2[0].x += a.x; acc2[0].y += a.y; acc2[1].x += a.z; acc2[1].y += a.w;
-            acc2[2].x += b.x; acc2[2].y += b.y; acc2[3].x += b.z; acc2[3].y += b.w;
-          }
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          if (act[k])
+            for (int r = 1; r < p.C; ++r) {
+              const float* q = s.red_in + (size_t)(r - 1) * h + col[k] * 8;
+              const float4 a = *reinterpret_cast<const float4*>(q);
+              const float4 b = *reinterpret_cast<const float4*>(q + 4);
+              acc2[k][0].x += a.x; acc2[k][0].y += a.y; acc2[k][1].x += a.z; acc2[k][1].y += a.w;
+              acc2[k][2].x += b.x; acc2[k][2].y += b.y; acc2[k][3].x += b.z; acc2[k][3].y += b.w;
+            }
       }
       ++n_red;
     }
-    if (rank == 0 && act) {
-      float4* dst = reinterpret_cast<float4*>(p.part + (size_t)cid * h + tid * 8);
-      __stcg(dst, make_float4(acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y));
-      __stcg(dst + 1, make_float4(acc2[2].x, acc2[2].y, acc2[3].x, acc2[3].y));
-    }
+    if (rank == 0)
+#pragma unroll
+      for (int k = 0; k < NCH; ++k)
+        if (act[k]) {
+          float4* dst = reinterpret_cast<float4*>(p.part + (size_t)cid * h + col[k] * 8);
+          __stcg(dst, make_float4(acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y));
+          __stcg(dst + 1, make_float4(acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y));
+        }
     // the fold's non-partial terms (x, biases) do not depend on the barrier:
     // fetch them now so their latency hides under it
     const int G = gridDim.x;
@@ -1101,7 +1140,9 @@ struct Consumer {
     consumer_sync(nct);
     stamp_layer(lrel, 5);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.f, 0.f);
+    for (int k = 0; k < NCH; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc2[k][i] = make_float2(0.f, 0.f);
   }
 
   // ---- main loop --------------------------------------------------------------
@@ -1112,20 +1153,23 @@ struct Consumer {
       cur_layer = l;
       const int lrel = l - p.l0;
       const LayerW& W = s.lw[lrel & 1];
-      float x[8];
+      float x[NCH][8];
       if (l == p.l0 && p.in_mode == IN_TOKEN) {
         const int tok = s.misc[2];
-        if (act) {
-          const uint4 w = __ldg(reinterpret_cast<const uint4*>(p.head.embed + (size_t)tok * h) + tid);
-          h8_to_f32(w, x);
-          if (blockIdx.x == 0) {
-            float4* dst = reinterpret_cast<float4*>(p.xs) + 2 * tid;
-            dst[0] = make_float4(x[0], x[1], x[2], x[3]);
-            dst[1] = make_float4(x[4], x[5], x[6], x[7]);
-          }
-        } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) x[i] = 0.f;
+        for (int k = 0; k < NCH; ++k) {
+          if (act[k]) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(p.head.embed + (size_t)tok * h) + col[k]);
+            h8_to_f32(w, x[k]);
+            if (blockIdx.x == 0) {
+              float4* dst = reinterpret_cast<float4*>(p.xs) + 2 * col[k];
+              dst[0] = make_float4(x[k][0], x[k][1], x[k][2], x[k][3]);
+              dst[1] = make_float4(x[k][4], x[k][5], x[k][6], x[k][7]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[k][i] = 0.f;
+          }
         }
       } else {
         load_vec(p.xs + (size_t)lrel * h, x);
@@ -1141,7 +1185,9 @@ struct Consumer {
       if (p.parallel) layer_norm(x, W.ln2g, W.ln2b, xn2);
       stamp_layer(lrel, 0);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.f, 0.f);
+      for (int k = 0; k < NCH; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc2[k][i] = make_float2(0.f, 0.f);
 
       const bool log_on = (TR && p.trace != nullptr) && tid == 0 && lrel == (p.l1 - p.l0) / 2;
       int n_log = 0;
@@ -1283,7 +1329,7 @@ struct Consumer {
           qkv_complete();
           attention_complete();
           reduce_event(1, lrel);
-          float r[8];
+          float r[NCH][8];
           load_vec(p.rbuf, r);
           layer_norm(r, W.ln2g, W.ln2b, xn2);
         } else if (dsc.type == ST_END) {
@@ -1313,13 +1359,15 @@ struct Consumer {
     const int h = p.h;
     stamp(4);
     const int L = p.l1 - p.l0;
-    float x[8];
+    float x[NCH][8];
     load_vec(p.xs + (size_t)L * h, x);
     if (p.head_mode == HEAD_LM) {
       layer_norm(x, p.head.lnfg, p.head.lnfb, xn1);
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) xn1[i] = make_float2(x[2 * i], x[2 * i + 1]);
+      for (int k = 0; k < NCH; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xn1[k][i] = make_float2(x[k][2 * i], x[k][2 * i + 1]);
     }
     for (;;) {
       const int sl = slot;
@@ -1370,8 +1418,8 @@ struct Consumer {
 // ===========================================================================
 // Kernel
 // ===========================================================================
-template <int DPL, int MAXT, bool TR>
-__global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
+template <int DPL, int NCH, bool TR>
+__global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Layout L = make_layout(p);
   const Smem s = carve(smem_raw, L, p);
@@ -1437,16 +1485,16 @@ __global__ void __launch_bounds__(MAXT, 1) decode_kernel(const Params p) {
     prod.mlp_c1 = s.misc[4];
     prod.run(pos, step & 1, rank, cid);
   } else if (warp < p.ncw) {
-    Consumer<DPL, TR> c(p, s, tid, rank, cid, pos, step);
+    Consumer<DPL, TR, NCH> c(p, s, tid, rank, cid, pos, step);
     c.run();
   }
   cluster_sync_all();
 }
 
-// Kernel variants: block <= 384 threads (hidden <= 2560) or <= 576 (hidden
-// <= 4096), each without / with the trace + measurement-debug paths compiled
-// in (variant = size + 2 * trace).
-#define NFB_VARIANTS(X) X(0, 384, false) X(1, 576, false) X(2, 384, true) X(3, 576, true)
+// Kernel variants: 1 or 2 hidden chunks per consumer thread (hidden <= 2560 /
+// <= 5120), each without / with the trace + measurement-debug paths compiled
+// in (variant = (NCH - 1) + 2 * trace).  Blocks are always <= 384 threads.
+#define NFB_VARIANTS(X) X(0, 1, false) X(1, 2, false) X(2, 1, true) X(3, 2, true)
 #define NFB_INST(i, t, tr) template __global__ void decode_kernel<8, t, tr>(const Params);
 NFB_VARIANTS(NFB_INST)
 

@@ -108,7 +108,7 @@ def test_fused_block_step_dropin_api():
         pkg.fused_block_step(bad, w, cache, 23, cfg, pkg.ClusterSpec(4), pkg.plan_full_fused())
 
 
-@pytest.mark.parametrize("cluster,max_clusters", [(1, 0), (2, 0), (4, 0), (2, 3), (8, 0)])
+@pytest.mark.parametrize("cluster,max_clusters", [(1, 0), (2, 0), (4, 0), (2, 3), (5, 0), (5, 3)])
 def test_cluster_decompositions_agree(cluster, max_clusters):
     """Every cluster size / cluster count (incl. several heads per cluster)
     gives the oracle's answer; KV split follows partition_kv."""
@@ -125,6 +125,15 @@ def test_cluster_decompositions_agree(cluster, max_clusters):
         got = eng.block_step(0, 37, x)
     want = O.block_step(x, O.f16_params(O.synth_block(s, 7)), O.KV.of(pk, pv), 37, s)
     assert scaled(got, want) <= TOL
+
+
+def test_cluster_size_must_leave_aligned_qkv_slices():
+    """The DSMEM bulk-copy exchange moves each rank's QKV slice as whole 16-byte
+    units: 3 * d_head / cluster_size must be a multiple of 4 (d 80: C = 8 gives 30)."""
+    cfg = P().ModelConfig(hidden=1280, n_heads=16, d_head=80, n_layers=1, d_mlp=5120,
+                          rotary_pct=0.25, vocab=64)
+    with pytest.raises(P()._lib.UnsupportedShapeError, match="multiple of 4 QKV rows"):
+        P().Engine(cfg, max_seq=64, cluster_size=8)
 
 
 def test_deterministic_bitwise():
@@ -244,3 +253,24 @@ def test_pythia_2p8b_wide_block_matches_reference():
         eng.kv_write(0, 0, pk, pv)
         out = eng.block_step(0, npre, xs[0])
     assert scaled(out, fx["outs"][0]) <= TOL
+
+
+@pytest.mark.slow
+def test_pythia_6p9b_wide_block_matches_oracle():
+    """BASELINE.json configs[2] shape (hidden 4096, d_head 128, d_mlp 16384):
+    one fused block step over a 64-position prefix vs the float64 oracle."""
+    cfg = P().preset("pythia-6.9b")
+    cfg = P().ModelConfig(hidden=cfg.hidden, n_heads=cfg.n_heads, d_head=cfg.d_head, n_layers=1,
+                          d_mlp=cfg.d_mlp, rotary_pct=cfg.rotary_pct, vocab=64)
+    s = O.Shape.of(cfg)
+    rng = np.random.default_rng(69)
+    npre = 64
+    pk = O.f16_round(rng.standard_normal((s.n_heads, npre, s.d_head)) * 0.5)
+    pv = O.f16_round(rng.standard_normal((s.n_heads, npre, s.d_head)) * 0.5)
+    x = rng.standard_normal(s.hidden) * 0.5
+    with P().Engine(cfg, max_seq=npre + 8) as eng:
+        eng.synth_block_weights(0, 3)
+        eng.kv_write(0, 0, pk, pv)
+        got = eng.block_step(0, npre, x)
+    want = O.block_step(x, O.f16_params(O.synth_block(s, 3)), O.KV.of(pk, pv), npre, s)
+    assert scaled(got, want) <= TOL
