@@ -3,6 +3,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -38,6 +41,46 @@ int fail(int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                            \
       return fail(NFB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
   } while (0)
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on first use (the library links no NCCL: single-GPU users need
+// none, and under torch the already-loaded libnccl.so.2 is reused).
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi& nccl_api() {
+  static NcclApi a;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
+      a.allReduce = (decltype(a.allReduce))dlsym(h, "ncclAllReduce");
+      a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+      a.getErrorString = (decltype(a.getErrorString))dlsym(h, "ncclGetErrorString");
+      a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.commDestroy && a.getErrorString;
+    }
+  }
+  return a;
+}
+
+#define NCK(expr)                                                                          \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess) return fail(NFB_ECUDA, std::string(#expr) + ": " + nccl_api().getErrorString(r_)); \
+  } while (0)
+
+
 
 // ---------------------------------------------------------------------------
 // binary16 round-to-nearest-even from float64 bits (IEEE 754; same results as
@@ -131,13 +174,44 @@ __global__ void synth_kernel(uint64_t seed, uint32_t stream, uint64_t n, int kin
 
 // KV prefix [H][count][d] -> cache [H][max_seq][d]
 __global__ void kv_synth_kernel(uint64_t seed, uint32_t stream, int H, int count, int d, int max_seq,
-                                uint16_t* out) {
-  const uint64_t n = (uint64_t)H * count * d;
+                                uint16_t* out, int head0 = 0) {
+  const uint64_t n = (uint64_t)H * count * d, base = (uint64_t)head0 * count * d;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t hh = i / ((uint64_t)count * d), rem = i % ((uint64_t)count * d);
-    out[hh * (uint64_t)max_seq * d + rem] = f64_to_f16_bits(synth_value(K_KV, uniform(seed, stream, i), 1.0));
+    out[hh * (uint64_t)max_seq * d + rem] =
+        f64_to_f16_bits(synth_value(K_KV, uniform(seed, stream, base + i), 1.0));
   }
+}
+
+// Slice [r0, r1) x [c0, c1) of a [R][K] tensor stream (element i = r * K + c
+// of the full tensor, nf/weights.py:58-62) -> fp16 / fp32, stored row-major
+// or transposed within the slice (tensor-parallel shards).
+__global__ void synth_slice_kernel(uint64_t seed, uint32_t stream, int64_t K, int64_t r0, int64_t r1, int64_t c0,
+                                   int64_t c1, int kind, double div, uint16_t* out16, float* out32,
+                                   int transpose) {
+  const int64_t nr = r1 - r0, nc = c1 - c0, n = nr * nc;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = r0 + j / nc, c = c0 + j % nc;
+    const uint16_t hb = f64_to_f16_bits(synth_value(kind, uniform(seed, stream, (uint64_t)(r * K + c)), div));
+    const int64_t idx = transpose ? (j % nc) * nr + j / nc : j;
+    if (out16) out16[idx] = hb;
+    else out32[idx] = f16_bits_to_f32(hb);
+  }
+}
+
+int launch_synth_slice(cudaStream_t st, uint64_t seed, uint32_t stream, int64_t K, int64_t r0, int64_t r1,
+                       int64_t c0, int64_t c1, int kind, double div, uint16_t* out16, float* out32,
+                       int transpose = 0) {
+  synth_slice_kernel<<<148 * 16, 256, 0, st>>>(seed, stream, K, r0, r1, c0, c1, kind, div, out16, out32,
+                                               transpose);
+  CK(cudaGetLastError());
+  return NFB_OK;
+}
+
+__global__ void advance_state_kernel(int* state) {
+  state[0] += 1;
+  state[1] += 1;
 }
 
 int launch_synth(cudaStream_t st, uint64_t seed, uint32_t stream, uint64_t n, int kind, double div,
@@ -180,6 +254,10 @@ struct nfb_ctx {
   float2* rope = nullptr;
   float *xs = nullptr, *rbuf = nullptr, *part = nullptr, *logits = nullptr;
   int *ctr = nullptr, *state = nullptr, *tokens = nullptr, *err = nullptr;
+  // tensor parallel (heads / FFN rows / vocab sharded over tp_size GPUs)
+  int tp_rank = 0, tp_size = 1;
+  nfb_model_desc full{};  // the unsharded model (desc holds this rank's shard)
+  void* nccl = nullptr;   // ncclComm_t
   unsigned long long* gbar = nullptr;
   unsigned long long* amax = nullptr;
   int ctr_stride = 0;
@@ -267,6 +345,10 @@ Params base_params(nfb_ctx* c) {
   p.pf_ahead = c->pf_ahead;
   p.mlp_gap = c->mlp_gap;
   p.pair = c->pair;
+  p.tp_root = c->tp_rank == 0 ? 1 : 0;
+  p.state_update = 1;
+  p.vocab_offset = c->tp_rank * c->desc.vocab;
+  p.vocab_full = c->full.vocab;
   p.debug = c->debug;
   return p;
 }
@@ -284,6 +366,48 @@ int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {
   if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
   return NFB_OK;
 }
+
+}  // namespace
+
+// One decode token under tensor parallelism: per layer a launch that leaves
+// this rank's split-K partial (rank 0: + residual + biases) in xs[l+1], then
+// an NCCL sum all-reduce of that [h] vector; the vocab-sharded LM head; a max
+// all-reduce of the packed (logit, ~index) argmax slots; the (pos, step)
+// advance.  Graph-capturable (NCCL supports stream capture).
+static int tp_token(nfb_ctx* c, cudaStream_t st) {
+  if (!c->nccl) return fail(NFB_ESTATE, "tensor-parallel context: call nfb_tp_init first");
+  if (c->trace || c->debug) return fail(NFB_EUNSUPPORTED, "tracing is single-launch only");
+  NcclApi& n = nccl_api();
+  const int L = c->desc.n_layers, h = c->desc.hidden;
+  for (int l = 0; l < L; ++l) {
+    Params p = base_params(c);
+    p.l0 = l;
+    p.l1 = l + 1;
+    p.xs = c->xs + (size_t)l * h;
+    p.in_mode = l == 0 ? IN_TOKEN : IN_X;
+    p.head_mode = HEAD_NONE;
+    p.advance_pos = 0;
+    p.state_update = 0;
+    TRY(launch(c, p, st));
+    NCK(n.allReduce(c->xs + (size_t)(l + 1) * h, c->xs + (size_t)(l + 1) * h, (size_t)h, ncclFloat32, ncclSum,
+                    (ncclComm_t)c->nccl, st));
+  }
+  Params p = base_params(c);
+  p.l0 = p.l1 = L;
+  p.xs = c->xs + (size_t)L * h;
+  p.in_mode = IN_X;
+  p.head_mode = HEAD_LM;
+  p.advance_pos = 0;
+  p.state_update = 0;
+  TRY(launch(c, p, st));
+  // both parity slots: the other one already holds identical values on every rank
+  NCK(n.allReduce(c->amax, c->amax, 2, ncclUint64, ncclMax, (ncclComm_t)c->nccl, st));
+  advance_state_kernel<<<1, 1, 0, st>>>(c->state);
+  CK(cudaGetLastError());
+  return NFB_OK;
+}
+
+namespace {
 
 int check_device_error(nfb_ctx* c) {
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -354,6 +478,9 @@ int check_layer(nfb_ctx* c, int layer) {
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+static bool g_creating_tp = false;  // nfb_create_tp: shard desc (hidden != local heads * d_head)
+static nfb_model_desc g_full_desc{};
+
 extern "C" {
 
 int nfb_version(void) { return 100; }
@@ -367,7 +494,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   const nfb_model_desc& m = *desc;
   if (m.hidden < 1 || m.n_heads < 1 || m.d_head < 1 || m.n_layers < 1 || m.d_mlp < 1 || m.vocab < 1)
     return fail(NFB_EINVAL, "model dimensions must be >= 1");
-  if (m.hidden != m.n_heads * m.d_head)
+  if (m.hidden != m.n_heads * m.d_head && !g_creating_tp)
     return fail(NFB_EINVAL, "hidden (" + std::to_string(m.hidden) + ") must equal n_heads * d_head (" +
                                 std::to_string(m.n_heads) + " * " + std::to_string(m.d_head) + ")");
   if (m.rotary_dims < 2 || m.rotary_dims % 2 || m.rotary_dims > m.d_head)
@@ -384,6 +511,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
 
   nfb_ctx* c = new nfb_ctx();
   c->desc = m;
+  c->full = g_creating_tp ? g_full_desc : m;
   c->device = device;
   c->max_seq = max_seq;
   c->C = C;
@@ -470,7 +598,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   }
   int r = NFB_OK;
   c->ctr_stride = L + 2;
-  if ((r = dalloc(c, &c->d_layers, L)) || (r = dalloc(c, &c->embed, (size_t)V * h)) ||
+  if ((r = dalloc(c, &c->d_layers, L)) || (r = dalloc(c, &c->embed, (size_t)c->full.vocab * h)) ||
       (r = dalloc(c, &c->unembed, (size_t)V * h)) || (r = dalloc(c, &c->lnfg, h)) ||
       (r = dalloc(c, &c->lnfb, h)) || (r = dalloc(c, &c->rope, (size_t)max_seq * (m.rotary_dims / 2))) ||
       (r = dalloc(c, &c->xs, (size_t)(L + 1) * h)) || (r = dalloc(c, &c->rbuf, h)) ||
@@ -507,6 +635,7 @@ int nfb_destroy(nfb_ctx* c) {
   if (!c) return NFB_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->nccl && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)c->nccl);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   for (void* p : c->allocs) cudaFree(p);
@@ -540,6 +669,7 @@ void* nfb_stream(nfb_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int nfb_set_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w, int dtype) {
   TRY(check_layer(c, layer));
+  if (c->tp_size > 1) return fail(NFB_EUNSUPPORTED, "tensor-parallel contexts take synthesized weights");
   if (!w) return fail(NFB_EINVAL, "null weights");
   const void* ptrs[12] = {w->ln1_gain, w->ln1_bias, w->qkv_weight, w->qkv_bias, w->out_weight, w->out_bias,
                           w->ln2_gain, w->ln2_bias, w->up_weight, w->up_bias, w->down_weight, w->down_bias};
@@ -570,6 +700,27 @@ int nfb_synth_block_weights(nfb_ctx* c, int layer, uint64_t seed) {
   const int64_t h = c->desc.hidden, m = c->desc.d_mlp;
   LayerBufs& b = c->layers[layer];
   cudaStream_t st = c->stream;
+  if (c->tp_size > 1) {
+    // this rank's shard of the full layer's streams: heads [hs, he), MLP rows [ms, me)
+    const int64_t d = c->desc.d_head, H = c->desc.n_heads, M = c->full.d_mlp;
+    const int64_t hs = c->tp_rank * H, he = hs + H, ms = c->tp_rank * m, me = ms + m;
+    const double sh = std::sqrt((double)h), sm = std::sqrt((double)M);
+    TRY(launch_synth(st, seed, 0, h, K_GAIN, 1.0, nullptr, b.ln1g));
+    TRY(launch_synth(st, seed, 1, h, K_LNBIAS, 1.0, nullptr, b.ln1b));
+    TRY(launch_synth_slice(st, seed, 2, h, hs * 3 * d, he * 3 * d, 0, h, K_WEIGHT, sh, b.wqkv, nullptr));
+    TRY(launch_synth_slice(st, seed, 3, 3 * h, 0, 1, hs * 3 * d, he * 3 * d, K_BIAS, 1.0, nullptr, b.bqkv));
+    TRY(launch_synth_slice(st, seed, 4, h, 0, h, hs * d, he * d, K_WEIGHT, sh, b.woT, nullptr, 1));
+    TRY(launch_synth(st, seed, 5, h, K_BIAS, 1.0, nullptr, b.bo));
+    TRY(launch_synth(st, seed, 6, h, K_GAIN, 1.0, nullptr, b.ln2g));
+    TRY(launch_synth(st, seed, 7, h, K_LNBIAS, 1.0, nullptr, b.ln2b));
+    TRY(launch_synth_slice(st, seed, 8, h, ms, me, 0, h, K_WEIGHT, sh, b.wup, nullptr));
+    TRY(launch_synth_slice(st, seed, 9, M, 0, 1, ms, me, K_BIAS, 1.0, nullptr, b.bup));
+    TRY(launch_synth_slice(st, seed, 10, M, 0, h, ms, me, K_WEIGHT, sm, b.wdT, nullptr, 1));
+    TRY(launch_synth(st, seed, 11, h, K_BIAS, 1.0, nullptr, b.bd));
+    CK(cudaStreamSynchronize(st));
+    b.weights = true;
+    return NFB_OK;
+  }
   // stream index = position in BlockWeights field order (nf/weights.py:55, 80-82)
   TRY(launch_synth(st, seed, 0, h, K_GAIN, 1.0, nullptr, b.ln1g));
   TRY(launch_synth(st, seed, 1, h, K_LNBIAS, 1.0, nullptr, b.ln1b));
@@ -632,6 +783,7 @@ int nfb_read_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w) {
 int nfb_set_head(nfb_ctx* c, const void* embed, const void* lnf_gain, const void* lnf_bias,
                  const void* unembed, int dtype) {
   if (!c) return fail(NFB_EINVAL, "null context");
+  if (c->tp_size > 1) return fail(NFB_EUNSUPPORTED, "tensor-parallel contexts take synthesized weights");
   cudaSetDevice(c->device);
   const size_t h = c->desc.hidden, V = c->desc.vocab;
   if (embed) {
@@ -656,10 +808,13 @@ int nfb_synth_head(nfb_ctx* c, uint64_t seed) {
   cudaSetDevice(c->device);
   const int64_t h = c->desc.hidden, V = c->desc.vocab;
   cudaStream_t st = c->stream;
-  TRY(launch_synth(st, seed, 0, V * h, K_PLAIN, 1.0, c->embed, nullptr));
+  // the embedding table is replicated (full vocab); the unembedding is this
+  // rank's vocab shard under tensor parallelism
+  TRY(launch_synth(st, seed, 0, (int64_t)c->full.vocab * h, K_PLAIN, 1.0, c->embed, nullptr));
   TRY(launch_synth(st, seed, 1, h, K_GAIN, 1.0, nullptr, c->lnfg));
   TRY(launch_synth(st, seed, 2, h, K_LNBIAS, 1.0, nullptr, c->lnfb));
-  TRY(launch_synth(st, seed, 3, V * h, K_WEIGHT, std::sqrt((double)h), c->unembed, nullptr));
+  TRY(launch_synth_slice(st, seed, 3, h, (int64_t)c->tp_rank * V, (int64_t)(c->tp_rank + 1) * V, 0, h, K_WEIGHT,
+                         std::sqrt((double)h), c->unembed, nullptr));
   CK(cudaStreamSynchronize(st));
   c->has_embed = c->has_lnf = c->has_unembed = true;
   return NFB_OK;
@@ -718,8 +873,9 @@ int nfb_kv_synth(nfb_ctx* c, int layer, int count, uint64_t seed) {
   const int H = c->desc.n_heads, d = c->desc.d_head;
   if (count) {
     const int grid = 148 * 8;
-    kv_synth_kernel<<<grid, 256, 0, c->stream>>>(seed, 0, H, count, d, c->max_seq, b.kc);
-    kv_synth_kernel<<<grid, 256, 0, c->stream>>>(seed, 1, H, count, d, c->max_seq, b.vc);
+    const int h0 = c->tp_rank * H;  // tensor parallel: this rank's heads of the full stream
+    kv_synth_kernel<<<grid, 256, 0, c->stream>>>(seed, 0, H, count, d, c->max_seq, b.kc, h0);
+    kv_synth_kernel<<<grid, 256, 0, c->stream>>>(seed, 1, H, count, d, c->max_seq, b.vc, h0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
   }
@@ -776,6 +932,8 @@ int nfb_block_step(nfb_ctx* c, int layer, int pos, const float* x_in, float* x_o
 int nfb_forward(nfb_ctx* c, int pos, const float* x_in, float* hidden_out, float* logits_out,
                 int head_mode) {
   if (!c || !x_in) return fail(NFB_EINVAL, "null argument");
+  if (c->tp_size > 1)
+    return fail(NFB_EUNSUPPORTED, "tensor-parallel contexts: use nfb_block_step per layer or the decode API");
   const int L = c->desc.n_layers, h = c->desc.hidden, V = c->desc.vocab;
   TRY(check_ready(c, 0, L, pos));
   TRY(check_finite(x_in, h));
@@ -811,7 +969,7 @@ int nfb_begin_decode(nfb_ctx* c, int pos, int token) {
   const int L = c->desc.n_layers;
   TRY(check_ready(c, 0, L, pos, true));  // may rewind: positions >= pos are discarded
   if (!c->has_embed || !c->has_unembed || !c->has_lnf) return fail(NFB_ESTATE, "embedding / LM head not set");
-  if (token < 0 || token >= c->desc.vocab) return fail(NFB_EINVAL, "token out of range");
+  if (token < 0 || token >= c->full.vocab) return fail(NFB_EINVAL, "token out of range");
   cudaSetDevice(c->device);
   CK(cudaStreamSynchronize(c->stream));
   int st[2] = {pos, 0};
@@ -836,6 +994,7 @@ static Params decode_params(nfb_ctx* c) {
 
 static int advance_host(nfb_ctx* c, int n) {
   if (c->decode_pos < 0) return fail(NFB_ESTATE, "call nfb_begin_decode first");
+  if (c->tp_size > 1 && !c->nccl) return fail(NFB_ESTATE, "tensor-parallel context: call nfb_tp_init first");
   if (c->decode_pos + n > c->max_seq) return fail(NFB_EINVAL, "decode would exceed the KV capacity");
   return NFB_OK;
 }
@@ -845,7 +1004,8 @@ int nfb_decode_step(nfb_ctx* c, void* stream) {
   TRY(advance_host(c, 1));
   cudaSetDevice(c->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-  TRY(launch(c, decode_params(c), st));
+  if (c->nccl) TRY(tp_token(c, st));  // tensor parallel (incl. a 1-rank communicator)
+  else TRY(launch(c, decode_params(c), st));
   c->decode_pos += 1;
   c->decode_step += 1;
   for (auto& b : c->layers) b.kv_len = c->decode_pos;
@@ -866,6 +1026,23 @@ int nfb_graph_capture(nfb_ctx* c) {
   // Resolve the cooperative fallback outside capture (a refused launch would
   // invalidate the capture).
   CK(cudaStreamSynchronize(c->stream));
+  if (c->nccl) {
+    // resolve the cooperative-launch fallback eagerly: one launch of layer 0
+    // as a plain block step is not needed -- tp_token's launch() handles it,
+    // so just capture the whole token sequence
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int r = tp_token(c, c->stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+    if (r != NFB_OK) {
+      if (g) cudaGraphDestroy(g);
+      return r;
+    }
+    if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("end capture: ") + cudaGetErrorString(e2));
+    c->graph = g;
+    CK(cudaGraphInstantiate(&c->gexec, g, 0));
+    return NFB_OK;
+  }
   const Params p = decode_params(c);
   const int variant = c->dpl + ((c->trace || c->debug) ? 2 : 0);
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -903,7 +1080,7 @@ int nfb_graph_replay(nfb_ctx* c, int n, void* stream) {
 
 int nfb_step_token(nfb_ctx* c, int token, int* next_token) {
   if (!c || !next_token) return fail(NFB_EINVAL, "null argument");
-  if (token < 0 || token >= c->desc.vocab) return fail(NFB_EINVAL, "token out of range");
+  if (token < 0 || token >= c->full.vocab) return fail(NFB_EINVAL, "token out of range");
   TRY(advance_host(c, 1));
   cudaSetDevice(c->device);
   const int par = c->decode_step & 1;
@@ -912,6 +1089,8 @@ int nfb_step_token(nfb_ctx* c, int token, int* next_token) {
   CK(cudaMemcpyAsync(c->amax + (par ^ 1), c->h_tok, 8, cudaMemcpyHostToDevice, c->stream));
   if (c->gexec) {
     CK(cudaGraphLaunch(c->gexec, c->stream));
+  } else if (c->nccl) {
+    TRY(tp_token(c, c->stream));
   } else {
     TRY(launch(c, decode_params(c), c->stream));
   }
@@ -1001,6 +1180,83 @@ int nfb_read_logits(nfb_ctx* c, float* out) {
   if (!c || !out) return fail(NFB_EINVAL, "null argument");
   TRY(nfb_sync(c));
   CK(cudaMemcpy(out, c->logits, (size_t)c->desc.vocab * 4, cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+
+int nfb_create_tp(const nfb_model_desc* full, int device, int max_seq, int cluster_size, int max_clusters,
+                  int tp_rank, int tp_size, nfb_ctx** out) {
+  if (!full || !out) return fail(NFB_EINVAL, "null argument");
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) return fail(NFB_EINVAL, "bad tensor-parallel rank / size");
+  if (full->n_heads % tp_size || full->d_mlp % tp_size || full->vocab % tp_size)
+    return fail(NFB_EUNSUPPORTED, "n_heads, d_mlp and vocab must divide by the tensor-parallel size");
+  if (tp_size > 1 && !full->parallel_residual)
+    return fail(NFB_EUNSUPPORTED, "tensor parallelism needs the parallel residual (one all-reduce per layer)");
+  nfb_model_desc m = *full;
+  m.n_heads /= tp_size;
+  m.d_mlp /= tp_size;
+  m.vocab /= tp_size;
+  g_creating_tp = true;
+  g_full_desc = *full;
+  const int r = nfb_create(&m, device, max_seq, cluster_size, max_clusters, out);
+  g_creating_tp = false;
+  if (r != NFB_OK) return r;
+  (*out)->tp_rank = tp_rank;
+  (*out)->tp_size = tp_size;
+  return NFB_OK;
+}
+
+int nfb_tp_unique_id(void* out128) {
+  if (!out128) return fail(NFB_EINVAL, "null argument");
+  NcclApi& n = nccl_api();
+  if (!n.ok) return fail(NFB_EUNSUPPORTED, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  NCK(n.getUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return NFB_OK;
+}
+
+int nfb_tp_init(nfb_ctx* c, const void* unique_id128) {
+  if (!c || !unique_id128) return fail(NFB_EINVAL, "null argument");
+  NcclApi& n = nccl_api();
+  if (!n.ok) return fail(NFB_EUNSUPPORTED, "libnccl.so.2 not found");
+  cudaSetDevice(c->device);
+  ncclUniqueId id;
+  memcpy(&id, unique_id128, sizeof(id));
+  ncclComm_t comm = nullptr;
+  NCK(n.commInitRank(&comm, c->tp_size, id, c->tp_rank));
+  c->nccl = comm;
+  return NFB_OK;
+}
+
+int nfb_tp_info(nfb_ctx* c, int* tp_rank, int* tp_size) {
+  if (!c || !tp_rank || !tp_size) return fail(NFB_EINVAL, "null argument");
+  *tp_rank = c->tp_rank;
+  *tp_size = c->tp_size;
+  return NFB_OK;
+}
+
+int nfb_head_logits(nfb_ctx* c, const float* h_in, float* logits_out, int head_mode) {
+  if (!c || !h_in || !logits_out) return fail(NFB_EINVAL, "null argument");
+  if (head_mode != NFB_HEAD_PROBE && head_mode != NFB_HEAD_LM) return fail(NFB_EINVAL, "bad head_mode");
+  if (!c->has_unembed) return fail(NFB_ESTATE, "unembedding not set");
+  if (head_mode == NFB_HEAD_LM && !c->has_lnf) return fail(NFB_ESTATE, "final LN not set");
+  const int L = c->desc.n_layers, h = c->desc.hidden, V = c->desc.vocab;
+  TRY(check_finite(h_in, h));
+  cudaSetDevice(c->device);
+  memcpy(c->h_x, h_in, (size_t)h * 4);
+  CK(cudaMemcpyAsync(c->xs + (size_t)L * h, c->h_x, (size_t)h * 4, cudaMemcpyHostToDevice, c->stream));
+  Params p = base_params(c);
+  p.l0 = p.l1 = L;
+  p.xs = c->xs + (size_t)L * h;
+  p.in_mode = IN_X;
+  p.head_mode = head_mode;
+  p.advance_pos = 0;
+  p.state_update = 0;
+  TRY(launch(c, p, c->stream));
+  CK(cudaMemcpyAsync(c->h_logits, c->logits, (size_t)V * 4, cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_device_error(c));
+  memcpy(logits_out, c->h_logits, (size_t)V * 4);
   return NFB_OK;
 }
 

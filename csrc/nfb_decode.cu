@@ -1063,6 +1063,10 @@ struct Consumer {
       reinterpret_cast<unsigned long long*>(&s.lw[(lrel + 1) & 1])[tid] =
           reinterpret_cast<const unsigned long long*>(&p.layers[cur_layer + 1])[tid];
     auto base_of = [&](int e) {
+      // tensor parallel: only the root rank adds the residual and the
+      // biases; the others contribute their split-K partial alone (the
+      // all-reduce after the launch sums the ranks)
+      if (!p.tp_root) return 0.f;
       if (event == 0) return __ldcg(xin + e) + __ldg(W.bo + e) + __ldg(W.bd + e);
       if (event == 1) return __ldcg(xin + e) + __ldg(W.bo + e);
       return __ldcg(p.rbuf + e) + __ldg(W.bd + e);
@@ -1074,7 +1078,7 @@ struct Consumer {
     stamp_layer(lrel, 8);
     if (tid == 0) {
       grid_sync(p.gbar, gridDim.x, p.err);
-      if (blockIdx.x == 0 && n_events == 0) {
+      if (blockIdx.x == 0 && n_events == 0 && p.state_update) {
         // every CTA has read (pos, step) before arriving: advance them now
         p.state[0] = pos + (p.advance_pos ? 1 : 0);
         p.state[1] = step + 1;
@@ -1392,7 +1396,7 @@ struct Consumer {
             const int row = lane < lm_n0 ? lm_a0 + lane : lm_a1 + lane - lm_n0;
             const float lg = row_total(s.wred + (gbuf * 2 * kRows + lane) * p.ncw);
             if (p.logits) p.logits[row] = lg;
-            const unsigned long long k = pack_argmax(lg, row);
+            const unsigned long long k = pack_argmax(lg, row + p.vocab_offset);
             best = k > best ? k : best;
           }
           gbuf ^= 1;
@@ -1447,7 +1451,7 @@ __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
     if (p.in_mode == IN_TOKEN) {
       const unsigned long long prev = *reinterpret_cast<volatile unsigned long long*>(p.amax + (par ^ 1));
       tok = (int)(0xffffffffu - (uint32_t)(prev & 0xffffffffull));
-      if (tok < 0 || tok >= p.V) tok = 0;
+      if (tok < 0 || tok >= p.vocab_full) tok = 0;
     }
     s.misc[2] = tok;
     s.misc[kMiscCum] = 0;
@@ -1456,7 +1460,8 @@ __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
     if (blockIdx.x == 0) {
       // Slots of the other parity are idle during this launch: reset them.
       for (int i = 0; i < p.ctr_stride; ++i) p.ctr[(par ^ 1) * p.ctr_stride + i] = 0;
-      if (p.head_mode != HEAD_NONE) p.amax[par] = 0ull;
+      // (the first layer launch of a step resets the step's argmax slot)
+      if (p.l0 == 0 && (p.head_mode != HEAD_NONE || p.in_mode == IN_TOKEN)) p.amax[par] = 0ull;
       if (p.in_mode == IN_TOKEN && step < p.max_seq) p.tokens[step] = tok;
     }
   }

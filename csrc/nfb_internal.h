@@ -78,6 +78,10 @@ struct Params {
   int pf_ahead;         // L2 prefetcher lead over the ring producer (bytes); 0 = off
   int mlp_gap;          // MLP pairs slotted after a head's QKV rows and after its KV share
   int pair;             // stage pairing (consumers take 2 ring stages per step): 1 MLP, 2 QKV, 4 W_out
+  int tp_root;          // 1: the fold adds residual + biases (single GPU, or tensor-parallel rank 0)
+  int state_update;     // 1: block 0 advances (pos, step) after the first grid barrier
+  int vocab_offset;     // global index of local unembedding row 0 (vocab-parallel LM head)
+  int vocab_full;       // embedding rows (= V unless the LM head is vocab-sharded)
   int debug;            // DBG_* bits (measurement only: results are garbage)
   // pointers
   const LayerW* layers;

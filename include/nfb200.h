@@ -150,6 +150,26 @@ int nfb_set_option(nfb_ctx* ctx, int option, int value);
 int nfb_read_trace(nfb_ctx* ctx, unsigned long long* out, int n);
 /* Block until the context stream is idle; reports device-side failures. */
 int nfb_sync(nfb_ctx* ctx);
+
+/* ---- tensor parallelism (Pythia-6.9B, BASELINE.json configs[2]) ----------
+ * Not in the reference (a single-process simulator): heads, FFN rows and the
+ * vocabulary are sharded over tp_size GPUs; each layer is one launch that
+ * leaves this rank's split-K partial (rank 0 adds residual + biases) and an
+ * NCCL all-reduce sums the ranks -- one per layer thanks to GPT-NeoX's
+ * parallel residual (nf/config.py:22, nf/golden.py:224-228).
+ * nfb_create_tp takes the FULL model description; the context holds shard
+ * tp_rank (weights only via nfb_synth_*; KV I/O addresses the local heads). */
+int nfb_create_tp(const nfb_model_desc* full, int device, int max_seq, int cluster_size,
+                  int max_clusters, int tp_rank, int tp_size, nfb_ctx** out);
+/* NCCL unique id (128 bytes) made on one rank, shared by the caller. */
+int nfb_tp_unique_id(void* out128);
+/* Join the tp_size-rank NCCL communicator; enables the decode API. */
+int nfb_tp_init(nfb_ctx* ctx, const void* unique_id128);
+int nfb_tp_info(nfb_ctx* ctx, int* tp_rank, int* tp_size);
+/* LM / probe head on a given final hidden state h_in[hidden] -> this
+ * context's logits (its vocab shard under TP).  Replaces the probe
+ * `unembed @ h` of DecodeInstance (nf/fidelity.py:139, 152). */
+int nfb_head_logits(nfb_ctx* ctx, const float* h_in, float* logits_out, int head_mode);
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
 

@@ -79,6 +79,11 @@ SIGNATURES = {
     "nfb_set_option": (_I, [_P, _I, _I]),
     "nfb_read_trace": (_I, [_P, C.POINTER(C.c_ulonglong), _I]),
     "nfb_stream": (_P, [_P]),
+    "nfb_create_tp": (_I, [C.POINTER(ModelDesc), _I, _I, _I, _I, _I, _I, C.POINTER(_P)]),
+    "nfb_tp_unique_id": (_I, [_P]),
+    "nfb_tp_init": (_I, [_P, _P]),
+    "nfb_tp_info": (_I, [_P, _IP, _IP]),
+    "nfb_head_logits": (_I, [_P, _FP, _FP, _I]),
 }
 
 _lib = None

@@ -40,8 +40,15 @@ def _host(a, dtype=None) -> np.ndarray:
 
 
 class Engine:
+    """``tp=(rank, size)`` makes a tensor-parallel shard of the full model
+    ``cfg`` (heads, FFN rows and vocabulary split over ``size`` GPUs; see
+    include/nfb200.h).  ``block_step`` then returns this rank's partial of the
+    layer output (rank 0: plus residual and biases) -- the sum over ranks is
+    the block output -- and ``tp_init`` joins the NCCL communicator that the
+    decode API all-reduces over."""
+
     def __init__(self, cfg, max_seq: int, gelu: str = "tanh", device: int = 0,
-                 cluster_size: int = 0, max_clusters: int = 0):
+                 cluster_size: int = 0, max_clusters: int = 0, tp: tuple[int, int] | None = None):
         if gelu not in ("tanh", "exact"):
             raise ValueError(f"unknown gelu variant {gelu!r} (use 'exact' or 'tanh')")
         self.lib = _lib.load()
@@ -50,8 +57,13 @@ class Engine:
                               cfg.rotary_dims, cfg.vocab, float(cfg.ln_eps), float(cfg.theta_base),
                               1 if cfg.parallel_residual else 0, 1 if gelu == "exact" else 0)
         h = C.c_void_p()
-        check(self.lib.nfb_create(C.byref(desc), device, self.max_seq, cluster_size, max_clusters,
-                                  C.byref(h)), "nfb_create")
+        self.tp = tuple(tp) if tp else (0, 1)
+        if tp:
+            check(self.lib.nfb_create_tp(C.byref(desc), device, self.max_seq, cluster_size, max_clusters,
+                                         int(tp[0]), int(tp[1]), C.byref(h)), "nfb_create_tp")
+        else:
+            check(self.lib.nfb_create(C.byref(desc), device, self.max_seq, cluster_size, max_clusters,
+                                      C.byref(h)), "nfb_create")
         self._h = h
         self._kv_len = [0] * cfg.n_layers
 
@@ -139,7 +151,7 @@ class Engine:
 
     def kv_read(self, layer: int, start: int = 0, count: int | None = None):
         count = self._kv_len[layer] - start if count is None else count
-        shape = (self.cfg.n_heads, count, self.cfg.d_head)
+        shape = (self.local_heads, count, self.cfg.d_head)
         k = np.empty(shape, np.float32)
         v = np.empty(shape, np.float32)
         check(self.lib.nfb_kv_read(self._h, layer, start, count, fptr(k), fptr(v)), "nfb_kv_read")
@@ -257,6 +269,32 @@ class Engine:
 
     def sync(self) -> None:
         check(self.lib.nfb_sync(self._h), "nfb_sync")
+
+
+    # ---- tensor parallelism ------------------------------------------------------
+    @staticmethod
+    def tp_unique_id() -> bytes:
+        """A fresh NCCL unique id (128 bytes), made on one rank and shared."""
+        lib = _lib.load()
+        buf = C.create_string_buffer(128)
+        check(lib.nfb_tp_unique_id(buf), "nfb_tp_unique_id")
+        return buf.raw
+
+    def tp_init(self, unique_id: bytes) -> None:
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(self.lib.nfb_tp_init(self._h, buf), "nfb_tp_init")
+
+    @property
+    def local_heads(self) -> int:
+        return self.cfg.n_heads // self.tp[1]
+
+    def head_logits(self, h, head: str = "lm") -> np.ndarray:
+        """LM (final LN + unembedding) or probe (unembedding only) logits of a
+        given final hidden state; under TP, this rank's vocabulary shard."""
+        x = _host(h, np.float32)
+        out = np.empty(self.cfg.vocab // self.tp[1], np.float32)
+        check(self.lib.nfb_head_logits(self._h, fptr(x), fptr(out), HEAD_MODES[head]), "nfb_head_logits")
+        return out
 
 
 def kv_seed(base: int, layer: int) -> int:

@@ -274,3 +274,77 @@ def test_pythia_6p9b_wide_block_matches_oracle():
         got = eng.block_step(0, npre, x)
     want = O.block_step(x, O.f16_params(O.synth_block(s, 3)), O.KV.of(pk, pv), npre, s)
     assert scaled(got, want) <= TOL
+
+
+# ---- tensor parallelism (BASELINE.json configs[2]) ---------------------------
+
+TP_CFG = dict(hidden=1280, n_heads=16, d_head=80, n_layers=2, d_mlp=5120, rotary_pct=0.25, vocab=512)
+
+
+def _tp_engines(cfg, size, npre, max_seq):
+    engs = [P().Engine(cfg, max_seq=max_seq, tp=(r, size)) for r in range(size)]
+    for e in engs:
+        for l in range(cfg.n_layers):
+            e.synth_block_weights(l, 100 + l)
+            e.kv_synth(l, npre, 7 + l)
+        e.synth_head(99)
+    return engs
+
+
+def test_tensor_parallel_shards_sum_to_the_full_block():
+    """Two TP shards on one GPU: the per-layer partials summed on the host
+    (what the NCCL all-reduce does) equal the unsharded engine, layer by layer;
+    each shard's KV append is its heads' slice; the vocab-sharded LM logits
+    concatenate to the full logits."""
+    cfg = P().ModelConfig(**TP_CFG)
+    npre, pos = 21, 21
+    full = P().Engine(cfg, max_seq=64)
+    for l in range(cfg.n_layers):
+        full.synth_block_weights(l, 100 + l)
+        full.kv_synth(l, npre, 7 + l)
+    full.synth_head(99)
+    shards = _tp_engines(cfg, 2, npre, 64)
+    x = np.random.default_rng(5).standard_normal(cfg.hidden) * 0.5
+    xf = xt = x
+    for l in range(cfg.n_layers):
+        xf = full.block_step(l, pos, xf)
+        xt = sum(e.block_step(l, pos, xt) for e in shards)
+        assert scaled(xt, xf) <= 1e-5
+        kf, vf = full.kv_read(l, pos, 1)
+        for r, e in enumerate(shards):
+            k, v = e.kv_read(l, pos, 1)
+            hs = slice(r * 8, (r + 1) * 8)
+            if l == 0:  # identical inputs: bit-identical fp16 K/V rows
+                assert np.array_equal(k, kf[hs]) and np.array_equal(v, vf[hs])
+            else:  # inputs differ by the fold order of the partial sums
+                assert scaled(k, kf[hs]) <= 1e-3 and scaled(v, vf[hs]) <= 1e-3
+    lf = full.head_logits(xf)
+    lt = np.concatenate([e.head_logits(xt) for e in shards])
+    assert scaled(lt, lf) <= 1e-5
+    for e in shards + [full]:
+        e.close()
+
+
+def test_tensor_parallel_decode_path_one_rank_nccl():
+    """The TP decode path (per-layer launches + NCCL all-reduces + sharded
+    head + state advance, graph-captured) on a 1-rank communicator reproduces
+    the fused single-launch decode token for token."""
+    cfg = P().ModelConfig(**TP_CFG)
+    npre = 16
+    ref = P().Engine(cfg, max_seq=64)
+    for l in range(cfg.n_layers):
+        ref.synth_block_weights(l, 100 + l)
+        ref.kv_synth(l, npre, 7 + l)
+    ref.synth_head(99)
+    tp = _tp_engines(cfg, 1, npre, 64)[0]
+    tp.tp_init(P().Engine.tp_unique_id())
+    out = []
+    for e in (ref, tp):
+        e.begin_decode(npre, token=3)
+        e.graph_capture()
+        e.graph_replay(6)
+        e.sync()
+        out.append(e.read_tokens(6))
+    assert list(out[0][0]) == list(out[1][0]) and out[0][1] == out[1][1]
+    tp.close()
+    ref.close()
