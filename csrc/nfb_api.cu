@@ -3,6 +3,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cublas_v2.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -19,6 +20,20 @@
 
 namespace nfb {
 const void* decode_kernel_ptr(int dpl);
+// batched decode kernels (csrc/nfb_batch.cu)
+__global__ void ln_hilo_kernel(const float* x, int B, int h, float eps, const float* g1, const float* b1,
+                               const float* g2, const float* b2, __half* a1, __half* a2);
+__global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, const int* state, int max_seq,
+                                 const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc);
+__global__ void attn_split_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
+                                  int max_seq, const int* state, float scale_log2, float* part);
+__global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx);
+__global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
+__global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
+                                const float* bd);
+__global__ void argmax_kernel(const float* lg, int B, int V, int* tokens, float* logits_out);
+__global__ void embed_kernel(const int* tokens, const __half* embed, int h, int V, float* x);
+__global__ void advance_pos_kernel(int* state);
 cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
                           bool cooperative);
 cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out);
@@ -258,6 +273,18 @@ struct nfb_ctx {
   int tp_rank = 0, tp_size = 1;
   nfb_model_desc full{};  // the unsharded model (desc holds this rank's shard)
   void* nccl = nullptr;   // ncclComm_t
+  // batched decode (nfb_batch_*): B sequences at one position, cuBLAS GEMMs
+  int bmax = 0, bcur = 0, bsplit = 1;
+  std::vector<uint16_t*> bkc, bvc;  // per layer [bmax][H][max_seq][d]
+  float *bx = nullptr, *by = nullptr, *bq = nullptr, *bpart = nullptr, *bz = nullptr, *bu = nullptr,
+        *bdn = nullptr, *blg = nullptr, *blogits = nullptr;
+  uint16_t *ba1 = nullptr, *ba2 = nullptr, *bctx = nullptr, *bg = nullptr;
+  int *btok = nullptr, *bstate = nullptr;
+  int bpos = -1;
+  void* cublas = nullptr;  // cublasHandle_t
+  void* cublas_ws = nullptr;
+  cudaGraph_t bgraph = nullptr;
+  cudaGraphExec_t bgexec = nullptr;
   unsigned long long* gbar = nullptr;
   unsigned long long* amax = nullptr;
   int ctr_stride = 0;
@@ -636,6 +663,9 @@ int nfb_destroy(nfb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->nccl && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)c->nccl);
+  if (c->bgexec) cudaGraphExecDestroy(c->bgexec);
+  if (c->bgraph) cudaGraphDestroy(c->bgraph);
+  if (c->cublas) cublasDestroy((cublasHandle_t)c->cublas);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   for (void* p : c->allocs) cudaFree(p);
@@ -1257,6 +1287,232 @@ int nfb_head_logits(nfb_ctx* c, const float* h_in, float* logits_out, int head_m
   CK(cudaMemcpyAsync(c->h_logits, c->logits, (size_t)V * 4, cudaMemcpyDeviceToHost, c->stream));
   TRY(check_device_error(c));
   memcpy(logits_out, c->h_logits, (size_t)V * 4);
+  return NFB_OK;
+}
+
+
+// ===========================================================================
+// Batched decode (BASELINE.json configs[3]): see csrc/nfb_batch.cu.
+// ===========================================================================
+static int bgemm(nfb_ctx* c, bool ta, int m, int n, int k, const uint16_t* A, int lda, const uint16_t* B, int ldb,
+                 float* C, int ldc) {
+  const float one = 1.f, zero = 0.f;
+  const cublasStatus_t st =
+      cublasGemmEx((cublasHandle_t)c->cublas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_OP_N, m, n, k, &one, A,
+                   CUDA_R_16F, lda, B, CUDA_R_16F, ldb, &zero, C, CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
+                   CUBLAS_GEMM_DEFAULT);
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(NFB_ECUDA, "cublasGemmEx failed (" + std::to_string((int)st) + ")");
+  return NFB_OK;
+}
+
+// One token for all bcur sequences: layers (LN -> QKV GEMM -> RoPE/append ->
+// split-KV attention -> W_out GEMM, LN2 -> up GEMM -> GELU -> down GEMM ->
+// residual) then final LN -> LM GEMM -> argmax.  in_token: x from btok.
+static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head) {
+  const nfb_model_desc& m = c->desc;
+  const int B = c->bcur, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
+  const int L = m.n_layers, S = c->bsplit;
+  cublasSetStream((cublasHandle_t)c->cublas, st);
+  if (in_token) embed_kernel<<<B, 256, 0, st>>>(c->btok, reinterpret_cast<const __half*>(c->embed), h, V, c->bx);
+  const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  for (int l = 0; l < L; ++l) {
+    const LayerBufs& w = c->layers[l];
+    ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g, w.ln2b,
+                                      reinterpret_cast<__half*>(c->ba1), reinterpret_cast<__half*>(c->ba2));
+    TRY(bgemm(c, true, 3 * h, 2 * B, h, w.wqkv, h, c->ba1, h, c->by, 3 * h));
+    attn_prep_kernel<<<dim3(B, H), 128, 3 * d * 4, st>>>(c->by, B, H, d, m.rotary_dims, c->bstate, c->max_seq,
+                                                         w.bqkv, c->rope, c->bq, reinterpret_cast<__half*>(c->bkc[l]),
+                                                         reinterpret_cast<__half*>(c->bvc[l]));
+    attn_split_kernel<<<dim3(B * H, S), 128, (d + 128 + 32) * 4, st>>>(
+        c->bq, reinterpret_cast<const __half*>(c->bkc[l]), reinterpret_cast<const __half*>(c->bvc[l]), B, H, d,
+        c->max_seq, c->bstate, scale_log2, c->bpart);
+    attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
+    TRY(bgemm(c, false, h, 2 * B, h, w.woT, h, c->bctx, h, c->bz, h));
+    TRY(bgemm(c, true, mm, 2 * B, h, w.wup, h, c->ba2, h, c->bu, mm));
+    gelu_hilo_kernel<<<dim3(B, (mm + 255) / 256), 256, 0, st>>>(c->bu, B, mm, w.bup, m.gelu_exact,
+                                                                reinterpret_cast<__half*>(c->bg));
+    TRY(bgemm(c, false, h, 2 * B, mm, w.wdT, h, c->bg, mm, c->bdn, h));
+    residual_kernel<<<dim3(B, (h + 255) / 256), 256, 0, st>>>(c->bx, B, h, c->bz, w.bo, c->bdn, w.bd);
+  }
+  if (head) {
+    ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, c->lnfg, c->lnfb, nullptr, nullptr,
+                                      reinterpret_cast<__half*>(c->ba1), nullptr);
+    TRY(bgemm(c, true, V, 2 * B, h, c->unembed, h, c->ba1, h, c->blg, V));
+    argmax_kernel<<<B, 1024, 0, st>>>(c->blg, B, V, c->btok, c->blogits);
+  }
+  advance_pos_kernel<<<1, 1, 0, st>>>(c->bstate);
+  CK(cudaGetLastError());
+  return NFB_OK;
+}
+
+int nfb_batch_init(nfb_ctx* c, int max_batch) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (max_batch < 1 || max_batch > 1024) return fail(NFB_EINVAL, "max_batch must be in [1, 1024]");
+  if (c->bmax) return fail(NFB_ESTATE, "batch buffers already allocated");
+  if (c->tp_size > 1) return fail(NFB_EUNSUPPORTED, "batched decode is single-GPU");
+  if (!c->desc.parallel_residual) return fail(NFB_EUNSUPPORTED, "batched decode needs the parallel residual");
+  if (c->desc.d_head > 128) return fail(NFB_EUNSUPPORTED, "batched decode needs d_head <= 128");
+  cudaSetDevice(c->device);
+  const nfb_model_desc& m = c->desc;
+  const size_t B = max_batch, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
+  // KV splits per (sequence, head): enough blocks to fill the GPU at B = 1
+  c->bsplit = std::max(1, std::min(64, (int)((2 * 148 * 8 + B * H - 1) / (B * H))));
+  c->bkc.resize(m.n_layers);
+  c->bvc.resize(m.n_layers);
+  int r = NFB_OK;
+  for (int l = 0; l < m.n_layers; ++l)
+    if ((r = dalloc(c, &c->bkc[l], B * H * c->max_seq * d)) || (r = dalloc(c, &c->bvc[l], B * H * c->max_seq * d)))
+      return r;
+  if ((r = dalloc(c, &c->bx, B * h)) || (r = dalloc(c, &c->by, 2 * B * 3 * h)) || (r = dalloc(c, &c->bq, B * h)) ||
+      (r = dalloc(c, &c->bpart, B * H * c->bsplit * (d + 2))) || (r = dalloc(c, &c->bz, 2 * B * h)) ||
+      (r = dalloc(c, &c->bu, 2 * B * mm)) || (r = dalloc(c, &c->bdn, 2 * B * h)) || (r = dalloc(c, &c->blg, 2 * B * V)) ||
+      (r = dalloc(c, &c->blogits, B * V)) || (r = dalloc(c, &c->ba1, 2 * B * h)) || (r = dalloc(c, &c->ba2, 2 * B * h)) ||
+      (r = dalloc(c, &c->bctx, 2 * B * h)) || (r = dalloc(c, &c->bg, 2 * B * mm)) || (r = dalloc(c, &c->btok, B)) ||
+      (r = dalloc(c, &c->bstate, 4)))
+    return r;
+  cublasHandle_t hb = nullptr;
+  if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) return fail(NFB_ECUDA, "cublasCreate failed");
+  c->cublas = hb;
+  const size_t ws = 32u << 20;
+  if (dalloc(c, reinterpret_cast<unsigned char**>(&c->cublas_ws), ws) != NFB_OK) return fail(NFB_ECUDA, "workspace");
+  cublasSetWorkspace(hb, c->cublas_ws, ws);  // fixed workspace: graph-capture safe
+  cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH);
+  c->bmax = max_batch;
+  return NFB_OK;
+}
+
+int nfb_batch_kv_synth(nfb_ctx* c, int count, uint64_t base_seed) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (!c->bmax) return fail(NFB_ESTATE, "call nfb_batch_init first");
+  if (count < 0 || count > c->max_seq) return fail(NFB_EINVAL, "KV synth count out of range");
+  cudaSetDevice(c->device);
+  const int H = c->desc.n_heads, d = c->desc.d_head;
+  for (int l = 0; l < c->desc.n_layers; ++l) {
+    // layer l: all bmax sequences as one stream of bmax * H heads (seed kv_seed(base, l))
+    const uint64_t seed = base_seed + 0x10000 + l;
+    if (count) {
+      kv_synth_kernel<<<148 * 8, 256, 0, c->stream>>>(seed, 0, H * c->bmax, count, d, c->max_seq, c->bkc[l]);
+      kv_synth_kernel<<<148 * 8, 256, 0, c->stream>>>(seed, 1, H * c->bmax, count, d, c->max_seq, c->bvc[l]);
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return NFB_OK;
+}
+
+int nfb_batch_kv_write(nfb_ctx* c, int layer, int seq, int start, int count, const void* keys, const void* values,
+                       int dtype) {
+  TRY(check_layer(c, layer));
+  if (!c->bmax) return fail(NFB_ESTATE, "call nfb_batch_init first");
+  if (seq < 0 || seq >= c->bmax || start < 0 || count < 0 || start + count > c->max_seq)
+    return fail(NFB_EINVAL, "batch KV write range invalid");
+  if (count && (!keys || !values)) return fail(NFB_EINVAL, "null keys/values");
+  cudaSetDevice(c->device);
+  const size_t H = c->desc.n_heads, d = c->desc.d_head;
+  if (count) {
+    std::vector<uint16_t> hk, hv;
+    TRY(to_f16_host(keys, dtype, H * count * d, hk));
+    TRY(to_f16_host(values, dtype, H * count * d, hv));
+    const size_t off = ((size_t)seq * H * c->max_seq + start) * d;
+    CK(cudaMemcpy2D(c->bkc[layer] + off, c->max_seq * d * 2, hk.data(), (size_t)count * d * 2, (size_t)count * d * 2,
+                    H, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(c->bvc[layer] + off, c->max_seq * d * 2, hv.data(), (size_t)count * d * 2, (size_t)count * d * 2,
+                    H, cudaMemcpyHostToDevice));
+  }
+  return NFB_OK;
+}
+
+static int batch_setup(nfb_ctx* c, int batch, int pos) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (!c->bmax) return fail(NFB_ESTATE, "call nfb_batch_init first");
+  if (batch < 1 || batch > c->bmax) return fail(NFB_EINVAL, "batch out of range");
+  if (pos < 0 || pos >= c->max_seq) return fail(NFB_EINVAL, "position out of range");
+  for (int l = 0; l < c->desc.n_layers; ++l)
+    if (!c->layers[l].weights) return fail(NFB_ESTATE, "weights of layer " + std::to_string(l) + " not set");
+  if (batch != c->bcur && c->bgexec) {
+    cudaGraphExecDestroy(c->bgexec);
+    c->bgexec = nullptr;
+  }
+  c->bcur = batch;
+  cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
+  int st[4] = {pos, 0, 0, 0};
+  CK(cudaMemcpy(c->bstate, st, sizeof(st), cudaMemcpyHostToDevice));
+  c->bpos = pos;
+  return NFB_OK;
+}
+
+int nfb_batch_forward(nfb_ctx* c, int batch, int pos, const float* x_in, float* x_out, float* logits_out) {
+  TRY(batch_setup(c, batch, pos));
+  if (!x_in) return fail(NFB_EINVAL, "null x");
+  if (logits_out && (!c->has_unembed || !c->has_lnf)) return fail(NFB_ESTATE, "LM head not set");
+  const size_t h = c->desc.hidden;
+  CK(cudaMemcpyAsync(c->bx, x_in, (size_t)batch * h * 4, cudaMemcpyHostToDevice, c->stream));
+  TRY(batch_token(c, c->stream, false, logits_out != nullptr));
+  if (x_out) CK(cudaMemcpyAsync(x_out, c->bx, (size_t)batch * h * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (logits_out)
+    CK(cudaMemcpyAsync(logits_out, c->blogits, (size_t)batch * c->desc.vocab * 4, cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_device_error(c));
+  c->bpos = pos + 1;
+  return NFB_OK;
+}
+
+int nfb_batch_begin(nfb_ctx* c, int batch, int pos, const int* tokens) {
+  TRY(batch_setup(c, batch, pos));
+  if (!tokens) return fail(NFB_EINVAL, "null tokens");
+  if (!c->has_embed || !c->has_unembed || !c->has_lnf) return fail(NFB_ESTATE, "embedding / LM head not set");
+  for (int b = 0; b < batch; ++b)
+    if (tokens[b] < 0 || tokens[b] >= c->full.vocab) return fail(NFB_EINVAL, "token out of range");
+  CK(cudaMemcpy(c->btok, tokens, (size_t)batch * 4, cudaMemcpyHostToDevice));
+  return NFB_OK;
+}
+
+int nfb_batch_step(nfb_ctx* c, int n, void* stream) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (!c->bcur || c->bpos < 0) return fail(NFB_ESTATE, "call nfb_batch_begin first");
+  if (n < 0 || c->bpos + n > c->max_seq) return fail(NFB_EINVAL, "batch decode would exceed the KV capacity");
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  for (int i = 0; i < n; ++i) {
+    if (c->bgexec) CK(cudaGraphLaunch(c->bgexec, st));
+    else TRY(batch_token(c, st, true, true));
+  }
+  c->bpos += n;
+  return NFB_OK;
+}
+
+int nfb_batch_graph_capture(nfb_ctx* c) {
+  if (!c) return fail(NFB_EINVAL, "null context");
+  if (!c->bcur) return fail(NFB_ESTATE, "call nfb_batch_begin first");
+  cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->bgexec) {
+    cudaGraphExecDestroy(c->bgexec);
+    c->bgexec = nullptr;
+  }
+  if (c->bgraph) {
+    cudaGraphDestroy(c->bgraph);
+    c->bgraph = nullptr;
+  }
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const int r = batch_token(c, c->stream, true, true);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+  if (r != NFB_OK) {
+    if (g) cudaGraphDestroy(g);
+    return r;
+  }
+  if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("end capture: ") + cudaGetErrorString(e2));
+  c->bgraph = g;
+  CK(cudaGraphInstantiate(&c->bgexec, g, 0));
+  return NFB_OK;
+}
+
+int nfb_batch_read_tokens(nfb_ctx* c, int* tokens) {
+  if (!c || !tokens) return fail(NFB_EINVAL, "null argument");
+  if (!c->bcur) return fail(NFB_ESTATE, "call nfb_batch_begin first");
+  TRY(nfb_sync(c));
+  CK(cudaMemcpy(tokens, c->btok, (size_t)c->bcur * 4, cudaMemcpyDeviceToHost));
   return NFB_OK;
 }
 

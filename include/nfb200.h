@@ -170,6 +170,25 @@ int nfb_tp_info(nfb_ctx* ctx, int* tp_rank, int* tp_size);
  * context's logits (its vocab shard under TP).  Replaces the probe
  * `unembed @ h` of DecodeInstance (nf/fidelity.py:139, 152). */
 int nfb_head_logits(nfb_ctx* ctx, const float* h_in, float* logits_out, int head_mode);
+
+/* ---- batched decode (BASELINE.json configs[3]: batch sweep 1/4/16/64) -------
+ * B sequences of one context (its weights) at the same position, each with its
+ * own KV cache.  Not in the reference (batch 1 only): the
+ * projections run as cuBLAS fp16 GEMMs on hi/lo activation rows, attention /
+ * RoPE / LN / GELU / residual / argmax in our kernels (csrc/nfb_batch.cu).
+ * Parallel residual only. */
+int nfb_batch_init(nfb_ctx* ctx, int max_batch);
+/* Synthetic prefix of every layer for all max_batch sequences (seed kv_seed(base, l)). */
+int nfb_batch_kv_synth(nfb_ctx* ctx, int count, uint64_t base_seed);
+int nfb_batch_kv_write(nfb_ctx* ctx, int layer, int seq, int start, int count, const void* keys,
+                       const void* values, int dtype);
+/* One step of `batch` sequences from inputs x_in[batch][hidden] at `pos` (the
+ * K/V of pos are appended); x_out / logits_out (LM head) optional. */
+int nfb_batch_forward(nfb_ctx* ctx, int batch, int pos, const float* x_in, float* x_out, float* logits_out);
+int nfb_batch_begin(nfb_ctx* ctx, int batch, int pos, const int* tokens);
+int nfb_batch_step(nfb_ctx* ctx, int n, void* stream);
+int nfb_batch_graph_capture(nfb_ctx* ctx);
+int nfb_batch_read_tokens(nfb_ctx* ctx, int* tokens);
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
 

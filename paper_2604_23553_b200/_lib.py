@@ -84,6 +84,14 @@ SIGNATURES = {
     "nfb_tp_init": (_I, [_P, _P]),
     "nfb_tp_info": (_I, [_P, _IP, _IP]),
     "nfb_head_logits": (_I, [_P, _FP, _FP, _I]),
+    "nfb_batch_init": (_I, [_P, _I]),
+    "nfb_batch_kv_synth": (_I, [_P, _I, C.c_uint64]),
+    "nfb_batch_kv_write": (_I, [_P, _I, _I, _I, _I, _P, _P, _I]),
+    "nfb_batch_forward": (_I, [_P, _I, _I, _FP, _FP, _FP]),
+    "nfb_batch_begin": (_I, [_P, _I, _I, _IP]),
+    "nfb_batch_step": (_I, [_P, _I, _P]),
+    "nfb_batch_graph_capture": (_I, [_P]),
+    "nfb_batch_read_tokens": (_I, [_P, _IP]),
 }
 
 _lib = None

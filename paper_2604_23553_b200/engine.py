@@ -297,6 +297,48 @@ class Engine:
         return out
 
 
+    # ---- batched decode (BASELINE configs[3]) -------------------------------------
+    def batch_init(self, max_batch: int) -> None:
+        """Per-sequence KV caches and buffers for up to max_batch sequences."""
+        check(self.lib.nfb_batch_init(self._h, int(max_batch)), "nfb_batch_init")
+        self.max_batch = int(max_batch)
+
+    def batch_kv_synth(self, count: int, base_seed: int) -> None:
+        check(self.lib.nfb_batch_kv_synth(self._h, count, C.c_uint64(base_seed & (2**64 - 1))), "nfb_batch_kv_synth")
+
+    def batch_kv_write(self, layer: int, seq: int, start: int, keys, values) -> None:
+        k, v = _host(keys), _host(values)
+        v = v.astype(k.dtype, copy=False)
+        check(self.lib.nfb_batch_kv_write(self._h, layer, seq, start, k.shape[1], C.c_void_p(k.ctypes.data),
+                                          C.c_void_p(v.ctypes.data), _dtype_code(k)), "nfb_batch_kv_write")
+
+    def batch_forward(self, pos: int, xs, logits: bool = False):
+        """One step of xs [B][hidden] at position pos -> (out [B][hidden], logits [B][V] or None)."""
+        x = _host(xs, np.float32)
+        B = x.shape[0]
+        out = np.empty_like(x)
+        lg = np.empty((B, self.cfg.vocab), np.float32) if logits else None
+        check(self.lib.nfb_batch_forward(self._h, B, pos, fptr(x), fptr(out), fptr(lg) if logits else None),
+              "nfb_batch_forward")
+        return out, lg
+
+    def batch_begin(self, pos: int, tokens) -> None:
+        t = np.ascontiguousarray(np.asarray(tokens, np.int32))
+        check(self.lib.nfb_batch_begin(self._h, t.size, pos, t.ctypes.data_as(C.POINTER(C.c_int))),
+              "nfb_batch_begin")
+        self._batch = t.size
+
+    def batch_step(self, n: int = 1, stream: int = 0) -> None:
+        check(self.lib.nfb_batch_step(self._h, n, C.c_void_p(stream) if stream else None), "nfb_batch_step")
+
+    def batch_graph_capture(self) -> None:
+        check(self.lib.nfb_batch_graph_capture(self._h), "nfb_batch_graph_capture")
+
+    def batch_tokens(self) -> np.ndarray:
+        t = np.empty(self._batch, np.int32)
+        check(self.lib.nfb_batch_read_tokens(self._h, t.ctypes.data_as(C.POINTER(C.c_int))), "nfb_batch_read_tokens")
+        return t
+
 def kv_seed(base: int, layer: int) -> int:
     """Seed of the synthetic KV prefix of one layer."""
     return (base + 0x10000 + layer) & (2**64 - 1)

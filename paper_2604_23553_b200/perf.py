@@ -73,3 +73,18 @@ def flops_per_token(cfg, position: int) -> float:
     """2 FLOPs per weight MAC + 4*h*(position+1) attention FLOPs per layer."""
     c = count_params(cfg)
     return 2.0 * (c.non_embedding + c.unembedding) + 4.0 * cfg.hidden * cfg.n_layers * (position + 1)
+
+
+def batch_step_bytes(cfg, seq_len: int, batch: int, elem_size: int = DEFAULT_ELEM_SIZE) -> int:
+    """Algorithmic bytes of one batched decode step (configs[3]): the weights
+    and LM head once, the KV history (read 2*P*h, write 2*h per layer) and the
+    residual stream per sequence -- SURVEY.md §8(d) batch extension
+    ``weights_once + B * (KV(P) + activations)``."""
+    one = step_bytes(cfg, seq_len, elem_size)
+    h, L = cfg.hidden, cfg.n_layers
+    per_seq = L * (2 * seq_len * h * elem_size + 2 * h * elem_size + 2 * h * 4)
+    return one + (batch - 1) * per_seq
+
+
+def mean_batch_step_bytes(cfg, first_pos: int, steps: int, batch: int) -> float:
+    return sum(batch_step_bytes(cfg, p + 1, batch) for p in range(first_pos, first_pos + steps)) / steps
