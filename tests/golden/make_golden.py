@@ -168,7 +168,25 @@ def bytes_model():
     (OUT / "bytes.json").write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")
 
 
+def cli_fixture():
+    """The reference CLI's own golden fixture (`neoxfuse golden`, nf/cli.py:343-397)
+    for a 256-hidden, d_head 64 block: the JSON parity artefact the B200 path
+    replays (paper_2604_23553_b200.formats.replay_golden_fixture)."""
+    import argparse
+    from neoxfuse import cli
+    cfg = OUT / "_cli_fixture.cfg"
+    cfg.write_text("model.hidden=256\nmodel.n_heads=4\nmodel.d_head=64\nmodel.n_layers=1\n"
+                   "model.d_mlp=1024\nmodel.rotary_pct=0.25\nmodel.vocab=64\nrun.gelu=tanh\n")
+    try:
+        ns = argparse.Namespace(config=str(cfg), preset=None, out=str(OUT / "cli_golden_h256.json"),
+                                format="json", seed=21, seq_lens=None, steps=6)
+        cli.cmd_golden(ns)
+    finally:
+        cfg.unlink()
+
+
 if __name__ == "__main__":
+    cli_fixture()
     prng()
     half()
     synth()

@@ -402,3 +402,29 @@ def test_batched_greedy_decode_graph_matches_eager():
         toks.append(seq)
         eng.close()
     assert toks[0] == toks[1]
+
+
+# ---- on-disk formats ---------------------------------------
+
+def test_reference_cli_golden_fixture_replays_on_the_kernel():
+    """`neoxfuse golden` JSON (generated by the reference CLI) through the fused
+    block: outputs and cache within the parity bar."""
+    from paper_2604_23553_b200.formats import replay_golden_fixture
+    r = replay_golden_fixture(os.path.join(G, "cli_golden_h256.json"))
+    assert r.output_error <= TOL and r.cache_error <= TOL
+
+
+def test_weight_files_load_into_the_kernel(tmp_path):
+    """Reference manifest + float32 blob -> device (fp16 RNE) -> identical to
+    device-side synthesis of the same seed."""
+    from paper_2604_23553_b200.formats import load_block_weights
+    pkg = P()
+    cfg = pkg.ModelConfig(hidden=768, n_heads=12, d_head=64, n_layers=1, d_mlp=3072, rotary_pct=0.25, vocab=64)
+    w = pkg.synth_weights(cfg, 31)
+    pkg.save_weights(w, tmp_path / "m.json", tmp_path / "w.bin")
+    x = np.random.default_rng(2).standard_normal(768) * 0.5
+    with pkg.Engine(cfg, max_seq=8) as a, pkg.Engine(cfg, max_seq=8) as b:
+        load_block_weights(a, 0, tmp_path / "m.json", tmp_path / "w.bin")
+        b.synth_block_weights(0, 31)
+        # float32 blob -> fp16 vs float64 -> fp16: equal up to rare double-rounding ties
+        assert scaled(a.block_step(0, 0, x), b.block_step(0, 0, x)) <= 1e-4
