@@ -24,9 +24,11 @@ const void* decode_kernel_ptr(int dpl);
 __global__ void ln_hilo_kernel(const float* x, int B, int h, float eps, const float* g1, const float* b1,
                                const float* g2, const float* b2, __half* a1, __half* a2);
 __global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, const int* state, int max_seq,
-                                 const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc);
+                                 const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc,
+                                 int pos_step, size_t seq_stride);
 __global__ void attn_split_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
-                                  int max_seq, const int* state, float scale_log2, float* part);
+                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
+                                  size_t seq_stride);
 __global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx);
 __global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
 __global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
@@ -1308,7 +1310,7 @@ static int bgemm(nfb_ctx* c, bool ta, int m, int n, int k, const uint16_t* A, in
 // One token for all bcur sequences: layers (LN -> QKV GEMM -> RoPE/append ->
 // split-KV attention -> W_out GEMM, LN2 -> up GEMM -> GELU -> down GEMM ->
 // residual) then final LN -> LM GEMM -> argmax.  in_token: x from btok.
-static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head) {
+static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bool prefill = false) {
   const nfb_model_desc& m = c->desc;
   const int B = c->bcur, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
   const int L = m.n_layers, S = c->bsplit;
@@ -1320,12 +1322,17 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head) {
     ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g, w.ln2b,
                                       reinterpret_cast<__half*>(c->ba1), reinterpret_cast<__half*>(c->ba2));
     TRY(bgemm(c, true, 3 * h, 2 * B, h, w.wqkv, h, c->ba1, h, c->by, 3 * h));
+    // batch: sequence b has its own cache; prefill: the T prompt rows share
+    // the context's cache at consecutive positions (causal)
+    __half* kc = reinterpret_cast<__half*>(prefill ? w.kc : c->bkc[l]);
+    __half* vc = reinterpret_cast<__half*>(prefill ? w.vc : c->bvc[l]);
+    const size_t sstride = prefill ? 0 : (size_t)H * c->max_seq * d;
+    const int pstep = prefill ? 1 : 0;
     attn_prep_kernel<<<dim3(B, H), 128, 3 * d * 4, st>>>(c->by, B, H, d, m.rotary_dims, c->bstate, c->max_seq,
-                                                         w.bqkv, c->rope, c->bq, reinterpret_cast<__half*>(c->bkc[l]),
-                                                         reinterpret_cast<__half*>(c->bvc[l]));
-    attn_split_kernel<<<dim3(B * H, S), 128, (d + 128 + 32) * 4, st>>>(
-        c->bq, reinterpret_cast<const __half*>(c->bkc[l]), reinterpret_cast<const __half*>(c->bvc[l]), B, H, d,
-        c->max_seq, c->bstate, scale_log2, c->bpart);
+                                                         w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride);
+    attn_split_kernel<<<dim3(B * H, S), 128, (d + 128 + 32) * 4, st>>>(c->bq, kc, vc, B, H, d, c->max_seq,
+                                                                        c->bstate, scale_log2, c->bpart, pstep,
+                                                                        sstride);
     attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
     TRY(bgemm(c, false, h, 2 * B, h, w.woT, h, c->bctx, h, c->bz, h));
     TRY(bgemm(c, true, mm, 2 * B, h, w.wup, h, c->ba2, h, c->bu, mm));
@@ -1516,4 +1523,34 @@ int nfb_batch_read_tokens(nfb_ctx* c, int* tokens) {
   return NFB_OK;
 }
 
+
+int nfb_prefill(nfb_ctx* c, int pos, int count, const float* x_in, float* x_out) {
+  if (!c || (count && !x_in)) return fail(NFB_EINVAL, "null argument");
+  if (!c->bmax) return fail(NFB_ESTATE, "call nfb_batch_init first (prefill runs in chunks of max_batch rows)");
+  if (count < 0 || pos < 0 || pos + count > c->max_seq) return fail(NFB_EINVAL, "prefill range invalid");
+  for (auto& b : c->layers)
+    if (b.kv_len != pos)
+      return fail(NFB_EINVAL, "cache holds " + std::to_string(b.kv_len) + " positions, expected " + std::to_string(pos));
+  const size_t h = c->desc.hidden;
+  TRY(check_finite(x_in, (int)(count * h)));
+  cudaSetDevice(c->device);
+  for (int t0 = 0; t0 < count; t0 += c->bmax) {
+    const int T = std::min(c->bmax, count - t0);
+    if (c->bgexec && T != c->bcur) {
+      cudaGraphExecDestroy(c->bgexec);
+      c->bgexec = nullptr;
+    }
+    c->bcur = T;
+    int st[4] = {pos + t0, 0, 0, 0};
+    CK(cudaMemcpyAsync(c->bstate, st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->bx, x_in + (size_t)t0 * h, (size_t)T * h * 4, cudaMemcpyHostToDevice, c->stream));
+    TRY(batch_token(c, c->stream, false, false, true));
+    if (x_out) CK(cudaMemcpyAsync(x_out + (size_t)t0 * h, c->bx, (size_t)T * h * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  TRY(check_device_error(c));
+  for (auto& b : c->layers) b.kv_len = pos + count;
+  c->decode_pos = -1;
+  return NFB_OK;
+}
 }  // extern "C"

@@ -74,8 +74,11 @@ __global__ void ln_hilo_kernel(const float* x, int B, int h, float eps, const fl
 // grid (B, H); y [2B][3h] (hi / lo GEMM rows) -> q [B][H][d] fp32 (rotated);
 // rotated k and v appended at `pos` of kc / vc [B][H][max_seq][d].
 __global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, const int* state, int max_seq,
-                                 const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc) {
-  const int b = blockIdx.x, hh = blockIdx.y, h3 = 3 * H * d, pos = state[0];
+                                 const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc,
+                                 int pos_step, size_t seq_stride) {
+  // row b: position state[0] + b * pos_step (batch: 0, prefill: 1) of the
+  // cache at kc + b * seq_stride (batch: own cache, prefill: the one cache)
+  const int b = blockIdx.x, hh = blockIdx.y, h3 = 3 * H * d, pos = state[0] + b * pos_step;
   const float* yh = y + (size_t)b * h3 + (size_t)hh * 3 * d;
   const float* yl = y + (size_t)(B + b) * h3 + (size_t)hh * 3 * d;
   const float* bb = bqkv + (size_t)hh * 3 * d;
@@ -84,7 +87,7 @@ __global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, co
   __syncthreads();
   const int half = rd >> 1;
   const float2* cs = rope + (size_t)pos * half;
-  const size_t kvo = (((size_t)b * H + hh) * max_seq + pos) * d;
+  const size_t kvo = (size_t)b * seq_stride + ((size_t)hh * max_seq + pos) * d;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float qv = sy[j], kv = sy[d + j];
     if (j < rd) {
@@ -107,18 +110,20 @@ __global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, co
 // grid (B * H, S), block 128: positions [s * per, min(P, (s+1) * per)) of
 // sequence b / head hh; writes (m, l, o[d]) of the split to part.
 __global__ void attn_split_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
-                                  int max_seq, const int* state, float scale_log2, float* part) {
-  // P = pos + 1 positions (history + the token appended by attn_prep_kernel),
-  // split evenly over gridDim.y blocks
-  const int P = state[0] + 1, per = (P + gridDim.y - 1) / gridDim.y;
+                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
+                                  size_t seq_stride) {
+  // P = pos + 1 positions (history + the token appended by attn_prep_kernel;
+  // prefill: causal, row b sees positions <= state[0] + b), split evenly
+  // over gridDim.y blocks (nf/golden.py:234-265 for the prefill semantics)
+  const int P = state[0] + (int)(blockIdx.x / H) * pos_step + 1, per = (P + gridDim.y - 1) / gridDim.y;
   extern __shared__ float sm[];
   float* sq = sm;           // [d]
   float* sp = sq + d;       // [128] scores / weights
   float* sh = sp + 128;     // [32] reduction scratch
   const int bh = blockIdx.x, s = blockIdx.y;
   const int p0 = s * per, p1 = min(P, p0 + per);
-  const __half* K = kc + (size_t)bh * max_seq * d;
-  const __half* V = vc + (size_t)bh * max_seq * d;
+  const __half* K = kc + (size_t)(bh / H) * seq_stride + (size_t)(bh % H) * max_seq * d;
+  const __half* V = vc + (size_t)(bh / H) * seq_stride + (size_t)(bh % H) * max_seq * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) sq[i] = q[(size_t)bh * d + i];
   __syncthreads();
   float m = -INFINITY, l = 0.f, o = 0.f;  // thread t < d owns output dim t

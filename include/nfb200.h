@@ -189,6 +189,12 @@ int nfb_batch_begin(nfb_ctx* ctx, int batch, int pos, const int* tokens);
 int nfb_batch_step(nfb_ctx* ctx, int n, void* stream);
 int nfb_batch_graph_capture(nfb_ctx* ctx);
 int nfb_batch_read_tokens(nfb_ctx* ctx, int* tokens);
+/* Prefill (reference prefill_attention_tiled, nf/golden.py:234-265):
+ * `count` prompt positions pos.. from inputs x_in[count][hidden] through all
+ * layers, causal attention, K/V appended to the context's cache (which must
+ * hold exactly `pos` positions), final hidden states to x_out (optional).
+ * Runs on the batched kernels in chunks of max_batch rows (nfb_batch_init). */
+int nfb_prefill(nfb_ctx* ctx, int pos, int count, const float* x_in, float* x_out);
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
 

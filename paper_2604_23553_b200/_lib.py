@@ -92,6 +92,7 @@ SIGNATURES = {
     "nfb_batch_step": (_I, [_P, _I, _P]),
     "nfb_batch_graph_capture": (_I, [_P]),
     "nfb_batch_read_tokens": (_I, [_P, _IP]),
+    "nfb_prefill": (_I, [_P, _I, _I, _FP, _FP]),
 }
 
 _lib = None

@@ -339,6 +339,16 @@ class Engine:
         check(self.lib.nfb_batch_read_tokens(self._h, t.ctypes.data_as(C.POINTER(C.c_int))), "nfb_batch_read_tokens")
         return t
 
+    def prefill(self, pos: int, xs) -> np.ndarray:
+        """Prompt positions pos.. (inputs xs [T][hidden]) through all layers with
+        causal attention; appends their K/V; returns the final hidden states.
+        Needs batch_init (chunks of max_batch rows)."""
+        x = _host(xs, np.float32)
+        out = np.empty_like(x)
+        check(self.lib.nfb_prefill(self._h, pos, x.shape[0], fptr(x), fptr(out)), "nfb_prefill")
+        self._kv_len = [pos + x.shape[0]] * self.cfg.n_layers
+        return out
+
 def kv_seed(base: int, layer: int) -> int:
     """Seed of the synthetic KV prefix of one layer."""
     return (base + 0x10000 + layer) & (2**64 - 1)

@@ -377,8 +377,8 @@ def test_batched_forward_matches_per_sequence_fused_kernel():
             for l in range(s.n_layers):
                 e1.kv_write(l, 0, *kv[b][l])
             hid, logits = e1.forward(npre, xs[b], head="lm")
-        assert scaled(out[b], hid[-1]) <= 1e-4
-        assert scaled(lg[b], logits) <= 1e-4
+        assert scaled(out[b], hid[-1]) <= 1e-3  # (current token's K/V from the fp16 cache)
+        assert scaled(lg[b], logits) <= 1e-3
     eng.close()
 
 
@@ -428,3 +428,28 @@ def test_weight_files_load_into_the_kernel(tmp_path):
         b.synth_block_weights(0, 31)
         # float32 blob -> fp16 vs float64 -> fp16: equal up to rare double-rounding ties
         assert scaled(a.block_step(0, 0, x), b.block_step(0, 0, x)) <= 1e-4
+
+
+def test_prefill_matches_token_by_token_decode():
+    """Prefill of a 9-token prompt in chunks of 4 (causal attention over the
+    prompt, nf/golden.py:234-265) == the fused kernel run token by token:
+    final hidden state of every prompt position and the resulting KV cache."""
+    cfg = P().ModelConfig(**TP_CFG)
+    T = 9
+    xs = np.random.default_rng(23).standard_normal((T, cfg.hidden)) * 0.5
+    a = P().Engine(cfg, max_seq=32)
+    a.synth_model(5)
+    a.batch_init(4)
+    out = a.prefill(0, xs)
+    b = P().Engine(cfg, max_seq=32)
+    b.synth_model(5)
+    ref = np.array([b.forward(t, xs[t])[0][-1] for t in range(T)])
+    # the batched kernels read the current token's K/V back from the fp16
+    # cache (the fused kernel uses its fp32 values): ~1e-4 differences
+    assert scaled(out, ref) <= 1e-3
+    for l in range(cfg.n_layers):
+        ka, va = a.kv_read(l, 0, T)
+        kb, vb = b.kv_read(l, 0, T)
+        assert scaled(ka, kb) <= 1e-3 and scaled(va, vb) <= 1e-3
+    a.close()
+    b.close()
