@@ -271,6 +271,9 @@ struct nfb_ctx {
   float2* rope = nullptr;
   float *xs = nullptr, *rbuf = nullptr, *part = nullptr, *logits = nullptr;
   int *ctr = nullptr, *state = nullptr, *tokens = nullptr, *err = nullptr;
+  int assist = 0;  // QKV assist parts per head (0: off)
+  float* yg = nullptr;
+  unsigned *yflag = nullptr, *epoch = nullptr;
   // tensor parallel (heads / FFN rows / vocab sharded over tp_size GPUs)
   int tp_rank = 0, tp_size = 1;
   nfb_model_desc full{};  // the unsharded model (desc holds this rank's shard)
@@ -344,7 +347,7 @@ Params base_params(nfb_ctx* c) {
   p.C = c->C;
   p.n_clusters = c->n_clusters;
   p.ncw = c->ncw;
-  p.rows_qkv = 3 * m.d_head / c->C;
+  p.rows_qkv = 3 * m.d_head / (c->C + c->assist);
   p.rows_o = m.d_head / c->C;
   p.stage_rows = c->stage_rows;
   p.n_slots = c->n_slots;
@@ -367,6 +370,10 @@ Params base_params(nfb_ctx* c) {
   p.tokens = c->tokens;
   p.logits = c->logits;
   p.err = c->err;
+  p.assist = c->assist;
+  p.yg = c->yg;
+  p.yflag = c->yflag;
+  p.epoch = c->epoch;
   p.trace = c->trace;
   p.trace_stride = c->trace_stride;
   p.dyn_mlp = c->dyn_mlp;
@@ -593,6 +600,11 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
   if (getenv("NFB_MLP_GAP")) c->mlp_gap = atoi(getenv("NFB_MLP_GAP"));
   if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
+  if (getenv("NFB_ASSIST")) c->assist = atoi(getenv("NFB_ASSIST"));
+  // assist needs CTAs without heads, parts of a multiple of 4 rows, <= 8 parts
+  if (c->assist < 0 || c->assist > 6 || (3 * m.d_head) % (C + c->assist) || ((3 * m.d_head) / (C + c->assist)) % 4 ||
+      nc * C <= C * std::min(m.n_heads, nc))
+    c->assist = 0;
   c->n_clusters = nc;
   c->grid = nc * C;
 
@@ -634,7 +646,9 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
       (r = dalloc(c, &c->part, (size_t)nc * h)) || (r = dalloc(c, &c->logits, V)) ||
       (r = dalloc(c, &c->ctr, 2 * c->ctr_stride)) || (r = dalloc(c, &c->gbar, 2)) ||
       (r = dalloc(c, &c->state, 2)) || (r = dalloc(c, &c->amax, 2)) ||
-      (r = dalloc(c, &c->tokens, max_seq)) || (r = dalloc(c, &c->err, 1)))
+      (r = dalloc(c, &c->tokens, max_seq)) || (r = dalloc(c, &c->err, 1)) ||
+      (r = dalloc(c, &c->yg, (size_t)H * 3 * d)) || (r = dalloc(c, &c->yflag, (size_t)H * 8)) ||
+      (r = dalloc(c, &c->epoch, 1)))
     return bail(r);
   e = cudaMemcpy(c->d_layers, table.data(), sizeof(LayerW) * L, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return bail(fail(NFB_ECUDA, cudaGetErrorString(e)));

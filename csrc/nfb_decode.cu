@@ -36,7 +36,7 @@ namespace nfb {
 
 enum StageType : int {
   ST_QKV = 1, ST_KV = 2, ST_WO = 3, ST_UP = 4, ST_DOWN = 5,
-  ST_SYNC = 6, ST_END = 7, ST_LM = 8, ST_HEAD_END = 9
+  ST_SYNC = 6, ST_END = 7, ST_LM = 8, ST_HEAD_END = 9, ST_AQKV = 10
 };
 constexpr int F_LAST = 1;   // last stage of a head's QKV / KV / W_out group
 constexpr int F_FIRST = 2;  // first stage of a row-dot batch (QKV / UP / LM)
@@ -101,12 +101,30 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, cons
 // [start_g, start_{g+1}) with start_g proportional to the prefix of
 // max(0, T - headbytes_j), T = (all bytes of the layer) / G.
 // ===========================================================================
+// QKV assist (p.assist > 0): each head's 3d QKV rows are split into C + A
+// parts; the C cluster ranks compute parts 0..C-1 (exchanged through DSMEM),
+// A CTAs without heads compute the rest first thing in their layer and
+// publish them through global memory (yg + yflag, epoch-tagged).  The head
+// clusters' serial chain (QKV -> attention -> W_out) gets shorter.
+__device__ __forceinline__ int assist_first_cta(const Params& p) {
+  const int G = p.n_clusters * p.C, headc = p.C * min(p.H, p.n_clusters);
+  return headc < G ? headc : G;
+}
+__device__ __forceinline__ int assist_units(const Params& p, int g) {
+  const int G = p.n_clusters * p.C, f = assist_first_cta(p), G2 = G - f;
+  const int U = p.assist ? p.H * p.assist : 0;
+  if (g < f || G2 <= 0) return 0;
+  const int k = g - f;
+  return k < U ? (U - k + G2 - 1) / G2 : 0;
+}
+
 __device__ __forceinline__ long long head_stage_bytes(const Params& p, int k, int r, int pos) {
-  if (k >= p.H) return 0;
+  long long a = (long long)assist_units(p, k * p.C + r) * p.rows_qkv * p.h * 2;
+  if (k >= p.H) return a;
   const int nh = (p.H - k + p.n_clusters - 1) / p.n_clusters;
   const int cnt = pos / p.C + (r < pos % p.C ? 1 : 0);
   const long long b = (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
-  return b * p.head_weight_pct / 100;
+  return a + b * p.head_weight_pct / 100;
 }
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
@@ -278,6 +296,18 @@ struct Producer {
       log_on = lrel == (p.l1 - p.l0) / 2;
       int* ctr = p.ctr + par * p.ctr_stride + lrel;
       int next = mlp_c0;
+      if (p.assist) {
+        // assist units of this CTA: QKV part (C + a) of head u / A, first thing
+        const int g = (int)(cid * C + rank), G = p.n_clusters * C, f = assist_first_cta(p), G2 = G - f;
+        for (int u = g - f; g >= f && u < p.H * p.assist; u += G2) {
+          const int hh = u / p.assist, q0 = (C + u % p.assist) * p.rows_qkv;
+          for (int r = 0; r < p.rows_qkv; r += p.stage_rows) {
+            const int n = min(p.stage_rows, p.rows_qkv - r);
+            const int fl = (r == 0 ? F_FIRST : 0) | (r + n >= p.rows_qkv ? F_LAST : 0);
+            push(ST_AQKV, q0 + r, n, (u << 8) | fl, W.wqkv + (size_t)(hh * 3 * d + q0 + r) * h, n * rowb);
+          }
+        }
+      }
       for (int hh = (int)cid; hh < p.H; hh += p.n_clusters) {
         const int tag = hh << 8;
         // QKV rows of this head owned by this rank.
@@ -960,6 +990,8 @@ struct Consumer {
     stamp_layer(cur_layer - p.l0, 2);
   }
 
+  unsigned epoch_base = 0;  // yflag epochs of this launch: epoch_base + lrel + 1
+
   // ---- QKV exchange (split phase) ---------------------------------------------
   bool qkv_pending = false, att_pending = false;
   int pend_head = 0;
@@ -983,6 +1015,22 @@ struct Consumer {
     const int head = pend_head;
     long long t0 = tick();
     mbar_wait_u32(smem_u32(s.bar_qkv), n_qkv & 1, p.err, 11);
+    if (p.assist) {
+      // the assist parts of this head: rows [C * rows_qkv, 3d) from global memory
+      const unsigned want = epoch_base + (unsigned)(cur_layer - p.l0) + 1u;
+      if (tid < p.assist) {
+        unsigned* f = p.yflag + head * p.assist + tid;
+        if (ld_acquire_u32(f) != want) {
+          const unsigned long long w0 = globaltimer();
+          while (ld_acquire_u32(f) != want)
+            if (globaltimer() - w0 > kTimeoutNs) fail_timeout(p.err, 15);
+        }
+      }
+      consumer_sync(nct);
+      const int r0 = p.C * p.rows_qkv;
+      for (int t = tid; t < 3 * p.d - r0; t += nct) s.ybuf[r0 + t] = __ldcg(p.yg + (size_t)head * 3 * p.d + r0 + t);
+      consumer_sync(nct);
+    }
     tock(8, t0);
     t0 = tick();
     ++n_qkv;
@@ -1078,6 +1126,7 @@ struct Consumer {
     stamp_layer(lrel, 8);
     if (tid == 0) {
       grid_sync(p.gbar, gridDim.x, p.err);
+      if (blockIdx.x == 0 && n_events == 0) *p.epoch = epoch_base + (unsigned)(p.l1 - p.l0);  // never repeats
       if (blockIdx.x == 0 && n_events == 0 && p.state_update) {
         // every CTA has read (pos, step) before arriving: advance them now
         p.state[0] = pos + (p.advance_pos ? 1 : 0);
@@ -1152,6 +1201,7 @@ struct Consumer {
   // ---- main loop --------------------------------------------------------------
   __device__ __forceinline__ void run() {
     const int h = p.h;
+    epoch_base = (unsigned)s.misc[5];
     stamp(2);
     for (int l = p.l0; l < p.l1; ++l) {
       cur_layer = l;
@@ -1255,6 +1305,24 @@ struct Consumer {
             fence_proxy_async_smem();
             qkv_publish(head);
             tock(13, tq);
+          }
+        } else if (dsc.type == ST_AQKV) {
+          // assist part of head u / A: row-dots, then publish to global
+          if (dsc.flags & F_FIRST) pend = 0;
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
+          release(sl);
+          pend += dsc.n;
+          if (last) {
+            const int u = head, hh = u / p.assist, q0 = dsc.a + dsc.n - p.rows_qkv;
+            consumer_sync(nct);
+            float* yg = p.yg + (size_t)hh * 3 * p.d + q0;
+            for (int t = tid; t < p.rows_qkv; t += nct)
+              __stcg(yg + t, row_total(s.wred + t * p.ncw) + __ldg(W.bqkv + hh * 3 * p.d + q0 + t));
+            consumer_sync(nct);
+            if (tid == 0) {
+              __threadfence();
+              st_release_u32(p.yflag + u, epoch_base + (unsigned)lrel + 1u);
+            }
           }
         } else if (dsc.type == ST_KV) {
           qkv_complete();
@@ -1454,6 +1522,7 @@ __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
       if (tok < 0 || tok >= p.vocab_full) tok = 0;
     }
     s.misc[2] = tok;
+    s.misc[5] = (int)*reinterpret_cast<volatile unsigned*>(p.epoch);
     s.misc[kMiscCum] = 0;
     if (TR && p.trace != nullptr)
       for (int k = 8; k < 16; ++k) p.trace[(size_t)blockIdx.x * p.trace_stride + k] = 0;

@@ -98,6 +98,10 @@ struct Params {
   int* tokens;          // [max_seq] token consumed at each step
   float* logits;        // [V] or null
   int* err;             // device error word
+  int assist;           // QKV parts per head computed by CTAs without heads (0: off)
+  float* yg;            // [H][3d] assist QKV rows (+ bias)
+  unsigned* yflag;      // [H * assist] epoch of the rows in yg (release / acquire)
+  unsigned* epoch;      // [1] epoch base: advanced by the launch's layer count, never reset
   unsigned long long* trace;  // optional [grid][trace_stride] globaltimer stamps
   int trace_stride;
 };

@@ -222,6 +222,10 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Grid barrier over all CTAs of the grid (all co-resident: one CTA per SM,
 // launch checked against cudaOccupancyMaxActiveClusters).  The 64-bit arrival
 // counter only ever grows: every barrier instance adds exactly nblocks, so the
