@@ -1344,7 +1344,7 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     const int pstep = prefill ? 1 : 0;
     attn_prep_kernel<<<dim3(B, H), 128, 3 * d * 4, st>>>(c->by, B, H, d, m.rotary_dims, c->bstate, c->max_seq,
                                                          w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride);
-    attn_split_kernel<<<dim3(B * H, S), 128, (d + 128 + 32) * 4, st>>>(c->bq, kc, vc, B, H, d, c->max_seq,
+    attn_split_kernel<<<dim3(B * H, S), 128, (d + 128 + 32 + 16 * d) * 4, st>>>(c->bq, kc, vc, B, H, d, c->max_seq,
                                                                         c->bstate, scale_log2, c->bpart, pstep,
                                                                         sstride);
     attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));

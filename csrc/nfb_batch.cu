@@ -116,17 +116,20 @@ __global__ void attn_split_kernel(const float* q, const __half* kc, const __half
   // prefill: causal, row b sees positions <= state[0] + b), split evenly
   // over gridDim.y blocks (nf/golden.py:234-265 for the prefill semantics)
   const int P = state[0] + (int)(blockIdx.x / H) * pos_step + 1, per = (P + gridDim.y - 1) / gridDim.y;
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) float sm[];
   float* sq = sm;           // [d]
   float* sp = sq + d;       // [128] scores / weights
   float* sh = sp + 128;     // [32] reduction scratch
+  float* so = sh + 32;      // [16][d] P.V partials of the position groups
   const int bh = blockIdx.x, s = blockIdx.y;
   const int p0 = s * per, p1 = min(P, p0 + per);
   const __half* K = kc + (size_t)(bh / H) * seq_stride + (size_t)(bh % H) * max_seq * d;
   const __half* V = vc + (size_t)(bh / H) * seq_stride + (size_t)(bh % H) * max_seq * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) sq[i] = q[(size_t)bh * d + i];
   __syncthreads();
-  float m = -INFINITY, l = 0.f, o = 0.f;  // thread t < d owns output dim t
+  // P.V: thread = (8-dim chunk c, position group g): 16-byte V loads
+  const int cpr = d >> 3, ng = blockDim.x / cpr, c8 = threadIdx.x % cpr, grp = threadIdx.x / cpr;
+  float m = -INFINITY, l = 0.f, o8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int t0 = p0; t0 < p1; t0 += 128) {
     const int pos = t0 + threadIdx.x;
     float sc = -INFINITY;
@@ -151,16 +154,37 @@ __global__ void attn_split_kernel(const float* q, const __half* kc, const __half
     const float alpha = exp2f(m - mn);
     l = l * alpha + block_sum(pw, sh);  // (block_sum syncs: sp is visible below)
     m = mn;
-    if (threadIdx.x < d) {
-      float acc = o * alpha;
+    if (grp < ng) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o8[k] *= alpha;
       const int n = min(128, p1 - t0);
-      for (int i = 0; i < n; ++i) acc = fmaf(sp[i], __half2float(V[(size_t)(t0 + i) * d + threadIdx.x]), acc);
-      o = acc;
+      const uint4* vr = reinterpret_cast<const uint4*>(V + (size_t)t0 * d) + c8;
+#pragma unroll 4
+      for (int i = grp; i < n; i += ng) {
+        const uint4 w = __ldg(vr + (size_t)i * cpr);
+        const __half2* hp = reinterpret_cast<const __half2*>(&w);
+        const float pw2 = sp[i];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(hp[k]);
+          o8[2 * k] = fmaf(pw2, f.x, o8[2 * k]);
+          o8[2 * k + 1] = fmaf(pw2, f.y, o8[2 * k + 1]);
+        }
+      }
     }
     __syncthreads();
   }
+  // combine the position groups (fixed order) -> o[d]
+  if (grp < ng)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) so[grp * d + 8 * c8 + k] = o8[k];
+  __syncthreads();
   float* out = part + ((size_t)bh * gridDim.y + s) * (d + 2);
-  if (threadIdx.x < d) out[threadIdx.x] = o;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float t = 0.f;
+    for (int g = 0; g < ng; ++g) t += so[g * d + j];
+    out[j] = t;
+  }
   if (threadIdx.x == 0) {
     out[d] = m;
     out[d + 1] = l;
