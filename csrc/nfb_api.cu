@@ -601,6 +601,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (getenv("NFB_MLP_GAP")) c->mlp_gap = atoi(getenv("NFB_MLP_GAP"));
   if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
   if (getenv("NFB_ASSIST")) c->assist = atoi(getenv("NFB_ASSIST"));
+  if (getenv("NFB_DYN_MLP")) c->dyn_mlp = atoi(getenv("NFB_DYN_MLP")) ? 1 : 0;
   // assist needs CTAs without heads, parts of a multiple of 4 rows, <= 8 parts
   if (c->assist < 0 || c->assist > 6 || (3 * m.d_head) % (C + c->assist) || ((3 * m.d_head) / (C + c->assist)) % 4 ||
       nc * C <= C * std::min(m.n_heads, nc))
