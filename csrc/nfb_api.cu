@@ -1162,6 +1162,14 @@ int nfb_set_option(nfb_ctx* c, int option, int value) {
     }
   } else if (option == NFB_OPT_DYNAMIC_MLP) {
     c->dyn_mlp = value ? 1 : 0;
+  } else if (option == NFB_OPT_HEAD_WEIGHT) {
+    if (value < 0 || value > 1000) return fail(NFB_EINVAL, "head weight must be in [0, 1000] percent");
+    c->head_weight_pct = value;
+  } else if (option == NFB_OPT_ASSIST) {
+    const int C = c->C, d3 = 3 * c->desc.d_head;
+    if (value && (value > 6 || d3 % (C + value) || (d3 / (C + value)) % 4 || c->grid <= C * std::min(c->desc.n_heads, c->n_clusters)))
+      return fail(NFB_EUNSUPPORTED, "QKV assist needs CTAs without heads and parts of a multiple of 4 rows");
+    c->assist = value;
   } else if (option == NFB_OPT_PREFETCH_KB) {
     if (value < 0 || value > 65536) return fail(NFB_EINVAL, "prefetch lead must be in [0, 65536] KiB");
     c->pf_ahead = value * 1024;

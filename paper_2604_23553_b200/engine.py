@@ -251,10 +251,12 @@ class Engine:
         return pos.value, step.value
 
     def set_option(self, option: str, value) -> None:
-        """"trace" / "dynamic_mlp" (bool) or "prefetch_kb" (int, L2 prefetch lead)."""
+        """"trace" / "dynamic_mlp" (bool), "prefetch_kb" (L2 prefetch lead, KiB),
+        "head_weight" (static MLP split, percent) or "assist" (QKV assist parts)."""
         code = {"trace": _lib.OPT_TRACE, "dynamic_mlp": _lib.OPT_DYNAMIC_MLP,
-                "prefetch_kb": _lib.OPT_PREFETCH_KB}[option]
-        v = int(value) if option == "prefetch_kb" else int(bool(value))
+                "prefetch_kb": _lib.OPT_PREFETCH_KB, "head_weight": _lib.OPT_HEAD_WEIGHT,
+                "assist": _lib.OPT_ASSIST}[option]
+        v = int(value) if option in ("prefetch_kb", "head_weight", "assist") else int(bool(value))
         check(self.lib.nfb_set_option(self._h, code, v), "nfb_set_option")
 
     def read_trace(self) -> np.ndarray:
@@ -348,6 +350,33 @@ class Engine:
         check(self.lib.nfb_prefill(self._h, pos, x.shape[0], fptr(x), fptr(out)), "nfb_prefill")
         self._kv_len = [pos + x.shape[0]] * self.cfg.n_layers
         return out
+
+    def autotune(self, pos: int, token: int = 1, steps: int = 32,
+                 weights=(80, 100, 115, 130, 160)) -> dict:
+        """Pick the static MLP split weight with the fastest
+        graph-mode decode at position ``pos`` (``steps`` tokens per candidate,
+        best of two).  The split stays a fixed function of (pos, rank), so the
+        tuned context is still bitwise reproducible run to run.  Leaves the
+        decode state rewound to (pos, token)."""
+        import time
+        best = None
+        for w in weights:
+            self.set_option("head_weight", w)
+            self.begin_decode(pos, token)
+            self.graph_capture()
+            t = []
+            for _ in range(3):
+                self.begin_decode(pos, token)
+                self.sync()
+                a = time.perf_counter()
+                self.graph_replay(steps)
+                self.sync()
+                t.append(time.perf_counter() - a)
+            if best is None or min(t) < best[1]:
+                best = (w, min(t))
+        self.set_option("head_weight", best[0])
+        self.begin_decode(pos, token)
+        return {"head_weight": best[0], "ms_per_token": best[1] / steps * 1e3}
 
 def kv_seed(base: int, layer: int) -> int:
     """Seed of the synthetic KV prefix of one layer."""
