@@ -355,7 +355,7 @@ class Engine:
                  weights=(80, 100, 115, 130, 160)) -> dict:
         """Pick the static MLP split weight with the fastest
         graph-mode decode at position ``pos`` (``steps`` tokens per candidate,
-        best of two).  The split stays a fixed function of (pos, rank), so the
+        best of three).  The split stays a fixed function of (pos, rank), so the
         tuned context is still bitwise reproducible run to run.  Leaves the
         decode state rewound to (pos, token)."""
         import time
