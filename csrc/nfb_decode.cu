@@ -407,20 +407,6 @@ __device__ __forceinline__ float dot8x2(const uint4& w, const float2* x) {
   return (a.x + b.x) + (a.y + b.y);
 }
 
-__device__ __forceinline__ float dot8(const uint4& w, const float* x) {
-  float f[8];
-  h8_to_f32(w, f);
-  float a = f[0] * x[0];
-  float b = f[1] * x[1];
-  a = fmaf(f[2], x[2], a);
-  b = fmaf(f[3], x[3], b);
-  a = fmaf(f[4], x[4], a);
-  b = fmaf(f[5], x[5], b);
-  a = fmaf(f[6], x[6], a);
-  b = fmaf(f[7], x[7], b);
-  return a + b;
-}
-
 // Reduce-scatter of 8 per-lane values over a warp: afterwards lane l holds the
 // warp sum of row ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
 __device__ __forceinline__ float butterfly8(float* v, int lane) {
