@@ -307,7 +307,8 @@ struct nfb_ctx {
   int debug = 0;
   int pf_ahead = 0;  // L2 prefetcher lead (bytes); measured: no gain at C2
   int mlp_gap = 1;   // MLP pairs interleaved into the head schedule (split-phase cluster syncs)
-  int pair = 1;      // consumer stage pairing mask (1 MLP, 2 QKV, 4 W_out)
+  int fold_all = 1;  // see Params::fold_all
+  int pair = 7;      // consumer stage pairing mask (1 MLP, 2 QKV, 4 W_out)
   unsigned long long* h_tok = nullptr;  // pinned [2]
   std::vector<void*> allocs;
 };
@@ -381,6 +382,7 @@ Params base_params(nfb_ctx* c) {
   p.pf_ahead = c->pf_ahead;
   p.mlp_gap = c->mlp_gap;
   p.pair = c->pair;
+  p.fold_all = c->fold_all;
   p.tp_root = c->tp_rank == 0 ? 1 : 0;
   p.state_update = 1;
   p.vocab_offset = c->tp_rank * c->desc.vocab;
@@ -600,6 +602,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
   if (getenv("NFB_MLP_GAP")) c->mlp_gap = atoi(getenv("NFB_MLP_GAP"));
   if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
+  if (getenv("NFB_FOLD_ALL")) c->fold_all = atoi(getenv("NFB_FOLD_ALL")) ? 1 : 0;
   if (getenv("NFB_ASSIST")) c->assist = atoi(getenv("NFB_ASSIST"));
   if (getenv("NFB_DYN_MLP")) c->dyn_mlp = atoi(getenv("NFB_DYN_MLP")) ? 1 : 0;
   // assist needs CTAs without heads, parts of a multiple of 4 rows, <= 8 parts
@@ -644,7 +647,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
       (r = dalloc(c, &c->unembed, (size_t)V * h)) || (r = dalloc(c, &c->lnfg, h)) ||
       (r = dalloc(c, &c->lnfb, h)) || (r = dalloc(c, &c->rope, (size_t)max_seq * (m.rotary_dims / 2))) ||
       (r = dalloc(c, &c->xs, (size_t)(L + 1) * h)) || (r = dalloc(c, &c->rbuf, h)) ||
-      (r = dalloc(c, &c->part, (size_t)nc * h)) || (r = dalloc(c, &c->logits, V)) ||
+      (r = dalloc(c, &c->part, (size_t)nc * C * h)) || (r = dalloc(c, &c->logits, V)) ||
       (r = dalloc(c, &c->ctr, 2 * c->ctr_stride)) || (r = dalloc(c, &c->gbar, 2)) ||
       (r = dalloc(c, &c->state, 2)) || (r = dalloc(c, &c->amax, 2)) ||
       (r = dalloc(c, &c->tokens, max_seq)) || (r = dalloc(c, &c->err, 1)) ||

@@ -1040,8 +1040,9 @@ struct Consumer {
   // event 0: parallel END, 1: sequential SYNC (attention half), 2: sequential END
   __device__ __forceinline__ void reduce_event(int event, int lrel) {
     const int h = p.h;
-    // 1) split-K partials of the cluster -> rank 0 via DSMEM
-    if (p.C > 1) {
+    // 1) split-K partials of the cluster -> rank 0 via DSMEM (fold_all: every
+    //    CTA publishes its own partial and the fold sums G of them instead)
+    if (p.C > 1 && !p.fold_all) {
       if (rank != 0) {
         // stage the partial in this CTA's own red_in slot, then one bulk copy
         // into the same slot of rank 0 (complete_tx on rank 0's barrier)
@@ -1075,11 +1076,12 @@ struct Consumer {
       }
       ++n_red;
     }
-    if (rank == 0)
+    const int npart = p.fold_all ? (int)gridDim.x : p.n_clusters;
+    if (rank == 0 || p.fold_all)
 #pragma unroll
       for (int k = 0; k < NCH; ++k)
         if (act[k]) {
-          float4* dst = reinterpret_cast<float4*>(p.part + (size_t)cid * h + col[k] * 8);
+          float4* dst = reinterpret_cast<float4*>(p.part + (size_t)(p.fold_all ? blockIdx.x : cid) * h + col[k] * 8);
           __stcg(dst, make_float4(acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y));
           __stcg(dst + 1, make_float4(acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y));
         }
@@ -1135,14 +1137,14 @@ struct Consumer {
         if (e >= h) break;
         float t = 0.f;
         int k = 0;
-        for (; k + 8 <= p.n_clusters; k += 8) {
+        for (; k + 8 <= npart; k += 8) {
           float v[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) v[u] = __ldcg(p.part + (size_t)(k + u) * h + e);
 #pragma unroll
           for (int u = 0; u < 8; ++u) t += v[u];
         }
-        for (; k < p.n_clusters; ++k) t += __ldcg(p.part + (size_t)k * h + e);
+        for (; k < npart; ++k) t += __ldcg(p.part + (size_t)k * h + e);
         finish(e, base_of(e) + t);
       }
     } else {
@@ -1153,14 +1155,14 @@ struct Consumer {
           const int e = e0 + ee;
           if (e < h) {
             int k = kg;
-            for (; k + 3 * nkg < p.n_clusters; k += 4 * nkg) {
+            for (; k + 3 * nkg < npart; k += 4 * nkg) {
               float v[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) v[u] = __ldcg(p.part + (size_t)(k + u * nkg) * h + e);
 #pragma unroll
               for (int u = 0; u < 4; ++u) t += v[u];
             }
-            for (; k < p.n_clusters; k += nkg) t += __ldcg(p.part + (size_t)k * h + e);
+            for (; k < npart; k += nkg) t += __ldcg(p.part + (size_t)k * h + e);
           }
           s.fold[kg * epc + ee] = t;
         }

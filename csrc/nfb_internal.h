@@ -77,6 +77,7 @@ struct Params {
   int head_weight_pct;  // static schedule: head-stage bytes weighted by this / 100
   int pf_ahead;         // L2 prefetcher lead over the ring producer (bytes); 0 = off
   int mlp_gap;          // MLP pairs slotted after a head's QKV rows and after its KV share
+  int fold_all;         // 1: every CTA stores its own split-K partial (no cluster pre-reduce); fold over all CTAs
   int pair;             // stage pairing (consumers take 2 ring stages per step): 1 MLP, 2 QKV, 4 W_out
   int tp_root;          // 1: the fold adds residual + biases (single GPU, or tensor-parallel rank 0)
   int state_update;     // 1: block 0 advances (pos, step) after the first grid barrier
