@@ -1098,14 +1098,22 @@ struct Consumer {
     if (event != 1 && tid < (int)(sizeof(LayerW) / 8) && cur_layer + 1 < p.l1)
       reinterpret_cast<unsigned long long*>(&s.lw[(lrel + 1) & 1])[tid] =
           reinterpret_cast<const unsigned long long*>(&p.layers[cur_layer + 1])[tid];
+    // the residual input: the launch input (token embedding read directly:
+    // CTA 0's xs[0] copy is not ordered before this read) or the previous
+    // reduction's output
+    auto x_of = [&](int e) {
+      if (event == 2) return __ldcg(p.rbuf + e);
+      if (n_events == 0 && p.in_mode == IN_TOKEN) return __half2float(p.head.embed[(size_t)s.misc[2] * h + e]);
+      return __ldcg(xin + e);
+    };
     auto base_of = [&](int e) {
       // tensor parallel: only the root rank adds the residual and the
       // biases; the others contribute their split-K partial alone (the
       // all-reduce after the launch sums the ranks)
       if (!p.tp_root) return 0.f;
-      if (event == 0) return __ldcg(xin + e) + __ldg(W.bo + e) + __ldg(W.bd + e);
-      if (event == 1) return __ldcg(xin + e) + __ldg(W.bo + e);
-      return __ldcg(p.rbuf + e) + __ldg(W.bd + e);
+      if (event == 0) return x_of(e) + __ldg(W.bo + e) + __ldg(W.bd + e);
+      if (event == 1) return x_of(e) + __ldg(W.bo + e);
+      return x_of(e) + __ldg(W.bd + e);
     };
     float base = 0.f;
     if (nkg > 1 && tid < epc && e0 + tid < h) base = base_of(e0 + tid);
@@ -1154,15 +1162,18 @@ struct Consumer {
           float t = 0.f;
           const int e = e0 + ee;
           if (e < h) {
-            int k = kg;
-            for (; k + 3 * nkg < npart; k += 4 * nkg) {
-              float v[4];
+            // all of this thread's partials in one round of loads (148
+            // partials over >= 10 groups fit one 16-wide batch)
+            for (int k = kg; k < npart; k += 16 * nkg) {
+              float v[16];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) v[u] = __ldcg(p.part + (size_t)(k + u * nkg) * h + e);
+              for (int u = 0; u < 16; ++u) {
+                const int kk = k + u * nkg;
+                v[u] = kk < npart ? __ldcg(p.part + (size_t)kk * h + e) : 0.f;
+              }
 #pragma unroll
-              for (int u = 0; u < 4; ++u) t += v[u];
+              for (int u = 0; u < 16; ++u) t += v[u];
             }
-            for (; k < npart; k += nkg) t += __ldcg(p.part + (size_t)k * h + e);
           }
           s.fold[kg * epc + ee] = t;
         }
