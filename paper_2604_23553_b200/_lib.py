@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnfb200.so")
+# NFB_LIB: load another build of the library (A/B measurements in tools/)
+LIB_PATH = os.environ.get("NFB_LIB") or os.path.join(_HERE, "libnfb200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "nfb200.h")
 
 NFB_OK, NFB_EINVAL, NFB_ECUDA, NFB_ESTATE, NFB_EUNSUPPORTED, NFB_EDEVICE = 0, -1, -2, -3, -4, -5

@@ -64,8 +64,9 @@ def main():
            "kv_wait_us_head_ctas": float(np.median(tr[heads, 7]) / CYC),
            "att_phase_us_cta0": [float(tr[0, 8 + k]) / CYC for k in range(4)],
            "head_sections_us_per_layer_cta0": {k: float(tr[0, i]) / CYC / L for i, k in
-                                                zip(range(8, 14), ["qkv_wait", "kv_append_begin", "att_publish",
-                                                                   "att_wait", "att_merge", "qkv_combine_publish"])},
+                                                zip(range(8, 16), ["qkv_wait", "kv_append_begin", "att_publish",
+                                                                   "att_wait", "att_merge", "qkv_combine_publish",
+                                                                   "att_first_stage", "att_other_stages"])},
            "head_phase_us": float(rel(tr[:, 5].max()) - rel(tr[:, 4].min())),
            "layers": []}
     for l in range(L):
