@@ -26,10 +26,11 @@ __global__ void ln_hilo_kernel(const float* x, int B, int h, float eps, const fl
 __global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, const int* state, int max_seq,
                                  const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc,
                                  int pos_step, size_t seq_stride);
-__global__ void attn_split_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
-                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
-                                  size_t seq_stride);
 __global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx);
+__global__ void attn_tile_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
+                                 int max_seq, const int* state, float scale_log2, float* part, int pos_step,
+                                 size_t seq_stride);
+size_t attn_tile_smem(int d);
 __global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
 __global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
                                 const float* bd);
@@ -1356,9 +1357,8 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     const int pstep = prefill ? 1 : 0;
     attn_prep_kernel<<<dim3(B, H), 128, 3 * d * 4, st>>>(c->by, B, H, d, m.rotary_dims, c->bstate, c->max_seq,
                                                          w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride);
-    attn_split_kernel<<<dim3(B * H, S), 128, (d + 128 + 32 + 16 * d) * 4, st>>>(c->bq, kc, vc, B, H, d, c->max_seq,
-                                                                        c->bstate, scale_log2, c->bpart, pstep,
-                                                                        sstride);
+    attn_tile_kernel<<<dim3(B * H, S), 128, attn_tile_smem(d), st>>>(c->bq, kc, vc, B, H, d, c->max_seq, c->bstate,
+                                                                     scale_log2, c->bpart, pstep, sstride);
     attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
     TRY(bgemm(c, false, h, 2 * B, h, w.woT, h, c->bctx, h, c->bz, h));
     TRY(bgemm(c, true, mm, 2 * B, h, w.wup, h, c->ba2, h, c->bu, mm));
@@ -1388,8 +1388,16 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   cudaSetDevice(c->device);
   const nfb_model_desc& m = c->desc;
   const size_t B = max_batch, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
-  // KV splits per (sequence, head): enough blocks to fill the GPU at B = 1
-  c->bsplit = std::max(1, std::min(64, (int)((2 * 148 * 8 + B * H - 1) / (B * H))));
+  // KV tiles of 128 positions per (sequence, head) over the whole cache
+  // (positions come from device state, so the grid covers max_seq; tiles
+  // past the current length exit at once)
+  c->bsplit = (c->max_seq + 127) / 128;
+  if (c->bsplit > 256) return fail(NFB_EUNSUPPORTED, "batched decode needs max_seq <= 32768");
+  {
+    const cudaError_t e = cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)attn_tile_smem((int)d));
+    if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("attn_tile smem attribute: ") + cudaGetErrorString(e));
+  }
   c->bkc.resize(m.n_layers);
   c->bvc.resize(m.n_layers);
   int r = NFB_OK;

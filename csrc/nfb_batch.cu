@@ -9,7 +9,8 @@
 // the GEMMs is ours (nf/golden.py:189-228 semantics):
 //   ln_hilo_kernel        LN1 / LN2 (two-pass, nf/golden.py:34-40) -> hi/lo rows
 //   attn_prep_kernel      QKV bias, partial RoPE (nf/golden.py:68-92), K/V append
-//   attn_split_kernel     split-KV decode attention, online softmax per split
+//   attn_tile_kernel      decode attention over 128-position KV tiles (bulk-copied
+//                         to shared memory), one softmax state per tile
 //   attn_combine_kernel   log-sum-exp merge of the splits (nf/golden.py:128-136)
 //   gelu_hilo_kernel      up bias + GELU (nf/golden.py:156-166) -> hi/lo rows
 //   residual_kernel       x += W_o ctx + b_o + W_down g + b_down (parallel residual)
@@ -19,6 +20,7 @@
 #include <cstdint>
 
 #include "nfb_internal.h"
+#include "nfb_ptx.cuh"
 
 namespace nfb {
 
@@ -52,22 +54,61 @@ __device__ __forceinline__ void put_hilo(__half* hi, __half* lo, int i, float v)
   lo[i] = __float2half_rn(v - __half2float(a));
 }
 
-// grid B; x [B][h] fp32 -> A1 / A2 [2B][h] fp16 (rows b: hi, B + b: lo)
-__global__ void ln_hilo_kernel(const float* x, int B, int h, float eps, const float* g1, const float* b1,
-                               const float* g2, const float* b2, __half* a1, __half* a2) {
+// grid B, block 256; x [B][h] fp32 (h <= 4096) -> A1 / A2 [2B][h] fp16 (rows
+// b: hi, B + b: lo).  The row is read once into registers (4 float4 per
+// thread), the LN parameters are fetched before the two reductions.
+__device__ __forceinline__ float4 ld4(const float* p, int i4, bool ok) {
+  return ok ? __ldg(reinterpret_cast<const float4*>(p) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void put_hilo4(__half* hi, __half* lo, int i4, float4 v) {
+  const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
+  const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+  reinterpret_cast<__half2*>(hi)[2 * i4] = h0;
+  reinterpret_cast<__half2*>(hi)[2 * i4 + 1] = h1;
+  reinterpret_cast<__half2*>(lo)[2 * i4] = __floats2half2_rn(v.x - f0.x, v.y - f0.y);
+  reinterpret_cast<__half2*>(lo)[2 * i4 + 1] = __floats2half2_rn(v.z - f1.x, v.w - f1.y);
+}
+__global__ void __launch_bounds__(256) ln_hilo_kernel(const float* x, int B, int h, float eps, const float* g1,
+                                                      const float* b1, const float* g2, const float* b2, __half* a1,
+                                                      __half* a2) {
   __shared__ float sh[32];
-  const int b = blockIdx.x;
+  const int b = blockIdx.x, h4 = h >> 2;
   const float* xb = x + (size_t)b * h;
+  float4 v[4], G1[4], B1[4], G2[4], B2[4];
   float s = 0.f;
-  for (int i = threadIdx.x; i < h; i += blockDim.x) s += xb[i];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i4 = threadIdx.x + k * blockDim.x;
+    const bool ok = i4 < h4;
+    v[k] = ok ? __ldcg(reinterpret_cast<const float4*>(xb) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    G1[k] = ld4(g1, i4, ok);
+    B1[k] = ld4(b1, i4, ok);
+    G2[k] = ld4(g2, i4, ok && a2);
+    B2[k] = ld4(b2, i4, ok && a2);
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
   const float mu = block_sum(s, sh) / h;
   float q = 0.f;
-  for (int i = threadIdx.x; i < h; i += blockDim.x) q += (xb[i] - mu) * (xb[i] - mu);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (threadIdx.x + k * blockDim.x < h4) {
+      const float dx = v[k].x - mu, dy = v[k].y - mu, dz = v[k].z - mu, dw = v[k].w - mu;
+      q += (dx * dx + dy * dy) + (dz * dz + dw * dw);
+    }
   const float rstd = rsqrtf(block_sum(q, sh) / h + eps);
-  for (int i = threadIdx.x; i < h; i += blockDim.x) {
-    const float n = (xb[i] - mu) * rstd;
-    put_hilo(a1 + (size_t)b * h, a1 + (size_t)(B + b) * h, i, n * g1[i] + b1[i]);
-    if (a2) put_hilo(a2 + (size_t)b * h, a2 + (size_t)(B + b) * h, i, n * g2[i] + b2[i]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i4 = threadIdx.x + k * blockDim.x;
+    if (i4 >= h4) continue;
+    const float4 n = make_float4((v[k].x - mu) * rstd, (v[k].y - mu) * rstd, (v[k].z - mu) * rstd,
+                                 (v[k].w - mu) * rstd);
+    put_hilo4(a1 + (size_t)b * h, a1 + (size_t)(B + b) * h, i4,
+              make_float4(n.x * G1[k].x + B1[k].x, n.y * G1[k].y + B1[k].y, n.z * G1[k].z + B1[k].z,
+                          n.w * G1[k].w + B1[k].w));
+    if (a2)
+      put_hilo4(a2 + (size_t)b * h, a2 + (size_t)(B + b) * h, i4,
+                make_float4(n.x * G2[k].x + B2[k].x, n.y * G2[k].y + B2[k].y, n.z * G2[k].z + B2[k].z,
+                            n.w * G2[k].w + B2[k].w));
   }
 }
 
@@ -107,107 +148,130 @@ __global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, co
   }
 }
 
-// grid (B * H, S), block 128: positions [s * per, min(P, (s+1) * per)) of
-// sequence b / head hh; writes (m, l, o[d]) of the split to part.
-__global__ void attn_split_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
-                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
-                                  size_t seq_stride) {
-  // P = pos + 1 positions (history + the token appended by attn_prep_kernel;
-  // prefill: causal, row b sees positions <= state[0] + b), split evenly
-  // over gridDim.y blocks (nf/golden.py:234-265 for the prefill semantics)
-  const int P = state[0] + (int)(blockIdx.x / H) * pos_step + 1, per = (P + gridDim.y - 1) / gridDim.y;
-  extern __shared__ __align__(16) float sm[];
-  float* sq = sm;           // [d]
-  float* sp = sq + d;       // [128] scores / weights
-  float* sh = sp + 128;     // [32] reduction scratch
-  float* so = sh + 32;      // [16][d] P.V partials of the position groups
-  const int bh = blockIdx.x, s = blockIdx.y;
-  const int p0 = s * per, p1 = min(P, p0 + per);
-  const __half* K = kc + (size_t)(bh / H) * seq_stride + (size_t)(bh % H) * max_seq * d;
-  const __half* V = vc + (size_t)(bh / H) * seq_stride + (size_t)(bh % H) * max_seq * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) sq[i] = q[(size_t)bh * d + i];
-  __syncthreads();
-  // P.V: thread = (8-dim chunk c, position group g): 16-byte V loads
-  const int cpr = d >> 3, ng = blockDim.x / cpr, c8 = threadIdx.x % cpr, grp = threadIdx.x / cpr;
-  float m = -INFINITY, l = 0.f, o8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int t0 = p0; t0 < p1; t0 += 128) {
-    const int pos = t0 + threadIdx.x;
-    float sc = -INFINITY;
-    if (pos < p1) {
-      const uint4* kr = reinterpret_cast<const uint4*>(K + (size_t)pos * d);
-      float a = 0.f;
-      for (int c = 0; c < (d >> 3); ++c) {
-        const uint4 w = __ldg(kr + c);
-        const __half2* hp = reinterpret_cast<const __half2*>(&w);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = __half22float2(hp[i]);
-          a = fmaf(f.x, sq[8 * c + 2 * i], a);
-          a = fmaf(f.y, sq[8 * c + 2 * i + 1], a);
-        }
-      }
-      sc = a * scale_log2;
+// grid (B * H, S), block 128: one 128-position tile of sequence b / head hh.
+// The tile's K and V rows (contiguous in the cache) arrive by two bulk copies
+// (TMA engine, one mbarrier): the bytes in flight cost no registers, so every
+// resident block has its whole tile outstanding.  Scores, max, exp2 weights
+// and P.V from shared memory; writes the tile's (m, l, o[d]) to part.  Tiles
+// at or past P (the grid covers max_seq) write an empty state.
+constexpr int kTile = 128;
+__global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __half* kc, const __half* vc, int B,
+                                                        int H, int d, int max_seq, const int* state,
+                                                        float scale_log2, float* part, int pos_step,
+                                                        size_t seq_stride) {
+  const int bh = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const int P = state[0] + (bh / H) * pos_step + 1, p0 = s * kTile, n = min(kTile, P - p0);
+  float* out = part + ((size_t)bh * gridDim.y + s) * (d + 2);
+  if (n <= 0) {
+    if (tid == 0) {
+      out[d] = -INFINITY;
+      out[d + 1] = 0.f;
     }
-    const float mn = fmaxf(m, block_max(sc, sh));
-    const float pw = pos < p1 ? exp2f(sc - mn) : 0.f;
-    sp[threadIdx.x] = pw;
-    const float alpha = exp2f(m - mn);
-    l = l * alpha + block_sum(pw, sh);  // (block_sum syncs: sp is visible below)
-    m = mn;
-    if (grp < ng) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) o8[k] *= alpha;
-      const int n = min(128, p1 - t0);
-      const uint4* vr = reinterpret_cast<const uint4*>(V + (size_t)t0 * d) + c8;
-#pragma unroll 4
-      for (int i = grp; i < n; i += ng) {
-        const uint4 w = __ldg(vr + (size_t)i * cpr);
-        const __half2* hp = reinterpret_cast<const __half2*>(&w);
-        const float pw2 = sp[i];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __half22float2(hp[k]);
-          o8[2 * k] = fmaf(pw2, f.x, o8[2 * k]);
-          o8[2 * k + 1] = fmaf(pw2, f.y, o8[2 * k + 1]);
-        }
-      }
-    }
-    __syncthreads();
+    return;
   }
-  // combine the position groups (fixed order) -> o[d]
-  if (grp < ng)
+  extern __shared__ __align__(128) unsigned char tsm[];
+  __half* Ks = reinterpret_cast<__half*>(tsm);
+  __half* Vs = Ks + kTile * d;
+  float* sq = reinterpret_cast<float*>(Vs + kTile * d);  // [d]
+  float* sp = sq + d;                                    // [128] weights
+  float* sh = sp + kTile;                                // [32] reduction scratch
+  float* so = sh + 32;                                   // [16][d] P.V partials of the groups
+  uint64_t* bar = reinterpret_cast<uint64_t*>(so + 16 * d + 2);
+  const size_t base = (size_t)(bh / H) * seq_stride + ((size_t)(bh % H) * max_seq + p0) * d;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = (uint32_t)(n * d * 2);
+    mbar_arrive_expect_tx(bar, 2 * bytes);
+    const uint64_t pol = policy_evict_first();
+    bulk_g2s(Ks, kc + base, bytes, bar, pol);
+    bulk_g2s(Vs, vc + base, bytes, bar, pol);
+  }
+  for (int i = tid; i < d; i += blockDim.x) sq[i] = q[(size_t)bh * d + i];
+  __syncthreads();
+  while (!mbar_try_wait(bar, 0)) {
+  }
+  const int cpr = d >> 3;
+  float sc = -INFINITY;
+  if (tid < n) {
+    const uint4* kr = reinterpret_cast<const uint4*>(Ks + (size_t)tid * d);
+    float a = 0.f, a2 = 0.f;
+    for (int c = 0; c < cpr; ++c) {
+      const uint4 w = kr[c];
+      const __half2* hp = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(hp[i]);
+        a = fmaf(f.x, sq[8 * c + 2 * i], a);
+        a2 = fmaf(f.y, sq[8 * c + 2 * i + 1], a2);
+      }
+    }
+    sc = (a + a2) * scale_log2;
+  }
+  const float m = block_max(sc, sh);
+  const float pw = tid < n ? exp2f(sc - m) : 0.f;
+  sp[tid] = pw;
+  const float l = block_sum(pw, sh);  // (syncs: sp is visible below)
+  const int ng = blockDim.x / cpr, c8 = tid % cpr, grp = tid / cpr;
+  if (grp < ng) {
+    float o8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const uint4* vr = reinterpret_cast<const uint4*>(Vs) + c8;
+#pragma unroll 4
+    for (int i = grp; i < n; i += ng) {
+      const uint4 w = vr[(size_t)i * cpr];
+      const __half2* hp = reinterpret_cast<const __half2*>(&w);
+      const float pw2 = sp[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(hp[k]);
+        o8[2 * k] = fmaf(pw2, f.x, o8[2 * k]);
+        o8[2 * k + 1] = fmaf(pw2, f.y, o8[2 * k + 1]);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) so[grp * d + 8 * c8 + k] = o8[k];
+  }
   __syncthreads();
-  float* out = part + ((size_t)bh * gridDim.y + s) * (d + 2);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+  for (int j = tid; j < d; j += blockDim.x) {
     float t = 0.f;
     for (int g = 0; g < ng; ++g) t += so[g * d + j];
     out[j] = t;
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     out[d] = m;
     out[d + 1] = l;
   }
 }
 
-// grid B * H: merge S split states in split order -> ctx [2B][h] fp16 hi / lo
+size_t attn_tile_smem(int d) { return (size_t)2 * kTile * d * 2 + (size_t)(d + kTile + 32 + 16 * d + 2) * 4 + 8; }
+
+// grid B * H, block 128: merge the S split states in split order -> ctx
+// [2B][h] fp16 hi / lo.  All states are read in one round (thread s < S
+// fetches state s), then each context element sums its S terms.
 __global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx) {
-  const int bh = blockIdx.x, b = bh / H, hh = bh % H, h = H * d;
+  __shared__ float sw[256], sh[32];
+  const int bh = blockIdx.x, b = bh / H, hh = bh % H, h = H * d, tid = threadIdx.x;
   const float* pb = part + (size_t)bh * S * (d + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < S; ++s)
-    if (pb[s * (d + 2) + d + 1] > 0.f) M = fmaxf(M, pb[s * (d + 2) + d]);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float L = 0.f, o = 0.f;
-    for (int s = 0; s < S; ++s) {
-      const float* st = pb + s * (d + 2);
-      if (st[d + 1] > 0.f) {
-        const float f = exp2f(st[d] - M);
-        L += st[d + 1] * f;
-        o += st[j] * f;
-      }
+  float ms = -INFINITY;
+  for (int s = tid; s < S; s += blockDim.x) {
+    const float l = pb[s * (d + 2) + d + 1];
+    if (l > 0.f) {
+      ms = fmaxf(ms, pb[s * (d + 2) + d]);
     }
+  }
+  const float M = block_max(ms, sh);
+  float lsum = 0.f;
+  for (int s = tid; s < S; s += blockDim.x) {
+    const float l = pb[s * (d + 2) + d + 1];
+    const float f = l > 0.f ? exp2f(pb[s * (d + 2) + d] - M) : 0.f;
+    sw[s] = f;
+    lsum += l > 0.f ? l * f : 0.f;
+  }
+  const float L = block_sum(lsum, sh);  // (syncs: sw is visible below)
+  for (int j = tid; j < d; j += blockDim.x) {
+    float o = 0.f;
+#pragma unroll 8
+    for (int s = 0; s < S; ++s) o += sw[s] == 0.f ? 0.f : pb[s * (d + 2) + j] * sw[s];
     put_hilo(ctx + (size_t)b * h, ctx + (size_t)(B + b) * h, hh * d + j, o / L);
   }
 }

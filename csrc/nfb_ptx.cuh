@@ -71,7 +71,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-__device__ __noinline__ void fail_timeout(int* err, int code) {
+static __device__ __noinline__ void fail_timeout(int* err, int code) {
   atomicExch(err, code);
   __threadfence_system();
   asm volatile("trap;");
