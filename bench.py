@@ -292,7 +292,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     cfg = preset(MODEL)
     K, W = args.steps, max(args.warmup, 3)
-    max_seq = CONTEXT + max(K, W) + 8
+    max_seq = CONTEXT + max(K, W, 32) + 8  # 32: the autotune window
     if args.tp:
         # one model sharded over the world: same seeds on every rank
         from paper_2604_23553_b200.parallel import broadcast_bytes

@@ -31,6 +31,9 @@ __global__ void attn_tile_kernel(const float* q, const __half* kc, const __half*
                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
                                  size_t seq_stride);
 size_t attn_tile_smem(int d);
+size_t attn_combine_smem(int S, int d);
+int skinny_gemm(cudaStream_t st, const __half* W, const __half* A, float* Y, int M, int N, int K);
+void transpose_f16(cudaStream_t st, const __half* in, __half* out, int rows, int cols);
 __global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
 __global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
                                 const float* bd);
@@ -281,6 +284,10 @@ struct nfb_ctx {
   void* nccl = nullptr;   // ncclComm_t
   // batched decode (nfb_batch_*): B sequences at one position, cuBLAS GEMMs
   int bmax = 0, bcur = 0, bsplit = 1;
+  // skinny-GEMM layouts of W_out / W_down ([h][h], [h][d_mlp] row-major) for
+  // batches of <= 4 sequences, rebuilt when the weights change (wver)
+  std::vector<uint16_t*> bwo, bwd;
+  unsigned long long wver = 1, bt_ver = 0;
   std::vector<uint16_t*> bkc, bvc;  // per layer [bmax][H][max_seq][d]
   float *bx = nullptr, *by = nullptr, *bq = nullptr, *bpart = nullptr, *bz = nullptr, *bu = nullptr,
         *bdn = nullptr, *blg = nullptr, *blogits = nullptr;
@@ -720,6 +727,7 @@ void* nfb_stream(nfb_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int nfb_set_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w, int dtype) {
   TRY(check_layer(c, layer));
+  ++c->wver;
   if (c->tp_size > 1) return fail(NFB_EUNSUPPORTED, "tensor-parallel contexts take synthesized weights");
   if (!w) return fail(NFB_EINVAL, "null weights");
   const void* ptrs[12] = {w->ln1_gain, w->ln1_bias, w->qkv_weight, w->qkv_bias, w->out_weight, w->out_bias,
@@ -747,6 +755,7 @@ int nfb_set_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w, int
 
 int nfb_synth_block_weights(nfb_ctx* c, int layer, uint64_t seed) {
   TRY(check_layer(c, layer));
+  ++c->wver;
   cudaSetDevice(c->device);
   const int64_t h = c->desc.hidden, m = c->desc.d_mlp;
   LayerBufs& b = c->layers[layer];
@@ -1334,6 +1343,28 @@ static int bgemm(nfb_ctx* c, bool ta, int m, int n, int k, const uint16_t* A, in
   return NFB_OK;
 }
 
+// Y[n][m] = sum_k W[m][k] A[n][k]: our skinny tensor-core kernel for N <= 32
+// activation rows, cuBLAS otherwise.  Wt: the same weights stored transposed
+// ([K][M], the fused kernel's layout) for the cuBLAS call; W may be null.
+static int rgemm(nfb_ctx* c, cudaStream_t st, int M, int N, int K, const uint16_t* W, const uint16_t* Wt,
+                 const uint16_t* A, float* Y) {
+  if (W && skinny_gemm(st, reinterpret_cast<const __half*>(W), reinterpret_cast<const __half*>(A), Y, M, N, K) == 0)
+    return NFB_OK;
+  if (Wt) return bgemm(c, false, M, N, K, Wt, M, A, K, Y, M);
+  return bgemm(c, true, M, N, K, W, K, A, K, Y, M);
+}
+
+// (Re)build the row-major W_out / W_down copies after a weight change.
+static void batch_prepare(nfb_ctx* c, cudaStream_t st) {
+  if (c->bwo.empty() || c->bt_ver == c->wver) return;
+  const int h = c->desc.hidden, mm = c->desc.d_mlp;
+  for (int l = 0; l < c->desc.n_layers; ++l) {
+    transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].woT), reinterpret_cast<__half*>(c->bwo[l]), h, h);
+    transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].wdT), reinterpret_cast<__half*>(c->bwd[l]), mm, h);
+  }
+  c->bt_ver = c->wver;
+}
+
 // One token for all bcur sequences: layers (LN -> QKV GEMM -> RoPE/append ->
 // split-KV attention -> W_out GEMM, LN2 -> up GEMM -> GELU -> down GEMM ->
 // residual) then final LN -> LM GEMM -> argmax.  in_token: x from btok.
@@ -1342,13 +1373,17 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
   const int B = c->bcur, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
   const int L = m.n_layers, S = c->bsplit;
   cublasSetStream((cublasHandle_t)c->cublas, st);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusNone) batch_prepare(c, st);
   if (in_token) embed_kernel<<<B, 256, 0, st>>>(c->btok, reinterpret_cast<const __half*>(c->embed), h, V, c->bx);
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   for (int l = 0; l < L; ++l) {
     const LayerBufs& w = c->layers[l];
     ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g, w.ln2b,
                                       reinterpret_cast<__half*>(c->ba1), reinterpret_cast<__half*>(c->ba2));
-    TRY(bgemm(c, true, 3 * h, 2 * B, h, w.wqkv, h, c->ba1, h, c->by, 3 * h));
+    const bool sk = 2 * B <= 8 && !c->bwo.empty();
+    TRY(rgemm(c, st, 3 * h, 2 * B, h, w.wqkv, nullptr, c->ba1, c->by));
     // batch: sequence b has its own cache; prefill: the T prompt rows share
     // the context's cache at consecutive positions (causal)
     __half* kc = reinterpret_cast<__half*>(prefill ? w.kc : c->bkc[l]);
@@ -1359,18 +1394,19 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
                                                          w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride);
     attn_tile_kernel<<<dim3(B * H, S), 128, attn_tile_smem(d), st>>>(c->bq, kc, vc, B, H, d, c->max_seq, c->bstate,
                                                                      scale_log2, c->bpart, pstep, sstride);
-    attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
-    TRY(bgemm(c, false, h, 2 * B, h, w.woT, h, c->bctx, h, c->bz, h));
-    TRY(bgemm(c, true, mm, 2 * B, h, w.wup, h, c->ba2, h, c->bu, mm));
+    attn_combine_kernel<<<B * H, 128, attn_combine_smem(S, d), st>>>(c->bpart, S, B, H, d,
+                                                                      reinterpret_cast<__half*>(c->bctx));
+    TRY(rgemm(c, st, h, 2 * B, h, sk ? c->bwo[l] : nullptr, w.woT, c->bctx, c->bz));
+    TRY(rgemm(c, st, mm, 2 * B, h, w.wup, nullptr, c->ba2, c->bu));
     gelu_hilo_kernel<<<dim3(B, (mm + 255) / 256), 256, 0, st>>>(c->bu, B, mm, w.bup, m.gelu_exact,
                                                                 reinterpret_cast<__half*>(c->bg));
-    TRY(bgemm(c, false, h, 2 * B, mm, w.wdT, h, c->bg, mm, c->bdn, h));
+    TRY(rgemm(c, st, h, 2 * B, mm, sk ? c->bwd[l] : nullptr, w.wdT, c->bg, c->bdn));
     residual_kernel<<<dim3(B, (h + 255) / 256), 256, 0, st>>>(c->bx, B, h, c->bz, w.bo, c->bdn, w.bd);
   }
   if (head) {
     ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, c->lnfg, c->lnfb, nullptr, nullptr,
                                       reinterpret_cast<__half*>(c->ba1), nullptr);
-    TRY(bgemm(c, true, V, 2 * B, h, c->unembed, h, c->ba1, h, c->blg, V));
+    TRY(rgemm(c, st, V, 2 * B, h, c->unembed, nullptr, c->ba1, c->blg));
     argmax_kernel<<<B, 1024, 0, st>>>(c->blg, B, V, c->btok, c->blogits);
   }
   advance_pos_kernel<<<1, 1, 0, st>>>(c->bstate);
@@ -1397,10 +1433,20 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
     const cudaError_t e = cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)attn_tile_smem((int)d));
     if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("attn_tile smem attribute: ") + cudaGetErrorString(e));
+    const cudaError_t e2 = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)attn_combine_smem(c->bsplit, (int)d));
+    if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("combine smem attribute: ") + cudaGetErrorString(e2));
   }
   c->bkc.resize(m.n_layers);
   c->bvc.resize(m.n_layers);
   int r = NFB_OK;
+  if (2 * B <= 8) {
+    c->bwo.resize(m.n_layers);
+    c->bwd.resize(m.n_layers);
+    for (int l = 0; l < m.n_layers; ++l)
+      if ((r = dalloc(c, &c->bwo[l], h * h)) || (r = dalloc(c, &c->bwd[l], h * mm))) return r;
+    c->bt_ver = 0;
+  }
   for (int l = 0; l < m.n_layers; ++l)
     if ((r = dalloc(c, &c->bkc[l], B * H * c->max_seq * d)) || (r = dalloc(c, &c->bvc[l], B * H * c->max_seq * d)))
       return r;
@@ -1514,6 +1560,7 @@ int nfb_batch_step(nfb_ctx* c, int n, void* stream) {
   if (n < 0 || c->bpos + n > c->max_seq) return fail(NFB_EINVAL, "batch decode would exceed the KV capacity");
   cudaSetDevice(c->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  if (c->bgexec) batch_prepare(c, st);  // the graph reads the copies in place
   for (int i = 0; i < n; ++i) {
     if (c->bgexec) CK(cudaGraphLaunch(c->bgexec, st));
     else TRY(batch_token(c, st, true, true));
@@ -1535,6 +1582,7 @@ int nfb_batch_graph_capture(nfb_ctx* c) {
     cudaGraphDestroy(c->bgraph);
     c->bgraph = nullptr;
   }
+  batch_prepare(c, c->stream);
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   const int r = batch_token(c, c->stream, true, true);
   cudaGraph_t g = nullptr;
