@@ -245,39 +245,38 @@ __global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __
 
 size_t attn_tile_smem(int d) { return (size_t)2 * kTile * d * 2 + (size_t)(d + kTile + 32 + 16 * d + 2) * 4 + 8; }
 
-// grid B * H, block 128, dynamic smem S * (d + 2) floats: merge the S tile
-// states in tile order -> ctx [2B][h] fp16 hi / lo.  All states are staged
-// in shared memory in one round of independent loads.
+// grid B * H, block 128: merge the S split states in split order -> ctx
+// [2B][h] fp16 hi / lo.  All states are read in one round (thread s < S
+// fetches state s), then each context element sums its S terms.
 __global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx) {
-  extern __shared__ float cst[];  // [S][d + 2], then the S weights
-  __shared__ float sh[32];
+  __shared__ float sw[256], sh[32];
   const int bh = blockIdx.x, b = bh / H, hh = bh % H, h = H * d, tid = threadIdx.x;
-  const int n = S * (d + 2);
-  const float* pb = part + (size_t)bh * n;
-#pragma unroll 8
-  for (int i = tid; i < n; i += blockDim.x) cst[i] = __ldcg(pb + i);
-  __syncthreads();
-  float* sw = cst + n;
+  const float* pb = part + (size_t)bh * S * (d + 2);
   float ms = -INFINITY;
-  for (int s = tid; s < S; s += blockDim.x)
-    if (cst[s * (d + 2) + d + 1] > 0.f) ms = fmaxf(ms, cst[s * (d + 2) + d]);
+  for (int s = tid; s < S; s += blockDim.x) {
+    const float l = pb[s * (d + 2) + d + 1];
+    if (l > 0.f) {
+      ms = fmaxf(ms, pb[s * (d + 2) + d]);
+    }
+  }
   const float M = block_max(ms, sh);
   float lsum = 0.f;
   for (int s = tid; s < S; s += blockDim.x) {
-    const float l = cst[s * (d + 2) + d + 1];
-    const float f = l > 0.f ? exp2f(cst[s * (d + 2) + d] - M) : 0.f;
+    const float l = pb[s * (d + 2) + d + 1];
+    const float f = l > 0.f ? exp2f(pb[s * (d + 2) + d] - M) : 0.f;
     sw[s] = f;
     lsum += l > 0.f ? l * f : 0.f;
   }
   const float L = block_sum(lsum, sh);  // (syncs: sw is visible below)
   for (int j = tid; j < d; j += blockDim.x) {
     float o = 0.f;
-    for (int s = 0; s < S; ++s) o += sw[s] == 0.f ? 0.f : cst[s * (d + 2) + j] * sw[s];
+#pragma unroll 8
+    for (int s = 0; s < S; ++s) o += sw[s] == 0.f ? 0.f : pb[s * (d + 2) + j] * sw[s];
     put_hilo(ctx + (size_t)b * h, ctx + (size_t)(B + b) * h, hh * d + j, o / L);
   }
 }
 
-size_t attn_combine_smem(int S, int d) { return (size_t)(S * (d + 2) + S) * 4; }
+size_t attn_combine_smem(int, int) { return 0; }
 
 __device__ __forceinline__ float gelu_f(float x, int exact) {
   if (exact) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
