@@ -609,6 +609,9 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   if (getenv("NFB_DEBUG")) c->debug = atoi(getenv("NFB_DEBUG"));
   if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
   if (getenv("NFB_MLP_GAP")) c->mlp_gap = atoi(getenv("NFB_MLP_GAP"));
+  // QKV / W_out pairs pay at one chunk per thread (C2: +1.9 %) but cost the
+  // two-chunk variant registers (C3 at weight 80: 294 vs 335 tok/s)
+  if (c->dpl & 1) c->pair = 1;
   if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
   if (getenv("NFB_FOLD_ALL")) c->fold_all = atoi(getenv("NFB_FOLD_ALL")) ? 1 : 0;
   if (getenv("NFB_ASSIST")) c->assist = atoi(getenv("NFB_ASSIST"));

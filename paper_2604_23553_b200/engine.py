@@ -352,7 +352,7 @@ class Engine:
         return out
 
     def autotune(self, pos: int, token: int = 1, steps: int = 32,
-                 weights=(80, 100, 115, 130, 160)) -> dict:
+                 weights=(80, 90, 100, 115, 130, 160)) -> dict:
         """Pick the static MLP split weight with the fastest
         graph-mode decode at position ``pos`` (``steps`` tokens per candidate,
         best of three).  The split stays a fixed function of (pos, rank), so the
