@@ -389,7 +389,7 @@ Params base_params(nfb_ctx* c) {
   p.head_weight_pct = c->head_weight_pct;
   p.pf_ahead = c->pf_ahead;
   p.mlp_gap = c->mlp_gap;
-  p.pair = c->pair;
+  p.pair = (c->dpl & 1) ? (c->pair & 1) : c->pair;  // two-chunk variant: MLP pairs only (compiled out)
   p.fold_all = c->fold_all;
   p.tp_root = c->tp_rank == 0 ? 1 : 0;
   p.state_update = 1;

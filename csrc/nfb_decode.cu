@@ -1285,7 +1285,7 @@ struct Consumer {
             qbias = tid < p.rows_qkv ? __ldg(W.bqkv + head * 3 * p.d + (int)rank * p.rows_qkv + tid) : 0.f;
           }
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
-            if (pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn1, s.wred + pend * p.ncw);
+            if (NCH == 1 && pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn1, s.wred + pend * p.ncw);
             else rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
           }
           release(sl);
@@ -1351,7 +1351,7 @@ struct Consumer {
             c2[r] = r < dsc2.n ? s.ctx[dsc2.a + r] : 0.f;
           }
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
-            if (pair) rowacc_pair(sbuf, dsc.n, sbuf2, dsc2.n, c, c2);
+            if (NCH == 1 && pair) rowacc_pair(sbuf, dsc.n, sbuf2, dsc2.n, c, c2);
             else rowacc_stage(sbuf, dsc.n, c);
           }
           release(sl);
