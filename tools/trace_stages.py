@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 
 from paper_2604_23553_b200 import Engine, preset  # noqa: E402
 
-NAMES = {1: "QKV", 2: "KV", 3: "WO", 4: "UP", 5: "DOWN", 6: "SYNC", 7: "END", 8: "LM", 9: "HEND"}
+NAMES = {1: "QKV", 2: "KV", 3: "WO", 4: "UP", 5: "DOWN", 6: "SYNC", 7: "END", 8: "LM", 9: "HEND", 10: "AQKV", 11: "HKV"}
 MAXS = 64
 
 
