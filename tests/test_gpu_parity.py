@@ -352,13 +352,15 @@ def test_tensor_parallel_decode_path_one_rank_nccl():
 
 # ---- batched decode (BASELINE.json configs[3]) --------------------------------
 
-def test_batched_forward_matches_per_sequence_fused_kernel():
-    """B = 3 sequences with their own KV histories through the batched path
-    (cuBLAS GEMMs on hi/lo rows + our attention / LN / GELU kernels) vs the
-    batch-1 fused kernel run per sequence: final hidden states and LM logits."""
+@pytest.mark.parametrize("max_batch,B", [(4, 3), (16, 6)])
+def test_batched_forward_matches_per_sequence_fused_kernel(max_batch, B):
+    """B sequences with their own KV histories through the batched path (GEMMs
+    on hi/lo rows: our skinny mma.sync kernel at 2B <= 8, cuBLAS above; our
+    tiled attention / LN / GELU kernels) vs the batch-1 fused kernel run per
+    sequence: final hidden states and LM logits."""
     cfg = P().ModelConfig(**TP_CFG)
     s = O.Shape.of(cfg)
-    B, npre = 3, 19
+    npre = 19
     rng = np.random.default_rng(17)
     kv = [[(O.f16_round(rng.standard_normal((s.n_heads, npre, s.d_head)) * 0.5),
             O.f16_round(rng.standard_normal((s.n_heads, npre, s.d_head)) * 0.5)) for _ in range(s.n_layers)]
@@ -366,7 +368,7 @@ def test_batched_forward_matches_per_sequence_fused_kernel():
     xs = rng.standard_normal((B, s.hidden)) * 0.5
     eng = P().Engine(cfg, max_seq=64)
     eng.synth_model(5)
-    eng.batch_init(4)
+    eng.batch_init(max_batch)
     for b in range(B):
         for l in range(s.n_layers):
             eng.batch_kv_write(l, b, 0, *kv[b][l])
