@@ -176,8 +176,9 @@ int nfb_head_logits(nfb_ctx* ctx, const float* h_in, float* logits_out, int head
 /* ---- batched decode (BASELINE.json configs[3]: batch sweep 1/4/16/64) -------
  * B sequences of one context (its weights) at the same position, each with its
  * own KV cache.  Not in the reference (batch 1 only): the
- * projections run as cuBLAS fp16 GEMMs on hi/lo activation rows, attention /
- * RoPE / LN / GELU / residual / argmax in our kernels (csrc/nfb_batch.cu).
+ * projections run as fp16 GEMMs on hi/lo activation rows (our mma.sync kernel
+ * at 2B <= 8 rows, cuBLAS above), attention / RoPE / LN / GELU / residual /
+ * argmax in our kernels (csrc/nfb_batch.cu).
  * Parallel residual only. */
 int nfb_batch_init(nfb_ctx* ctx, int max_batch);
 /* Synthetic prefix of every layer for all max_batch sequences (seed kv_seed(base, l)). */
