@@ -31,7 +31,6 @@ __global__ void attn_tile_kernel(const float* q, const __half* kc, const __half*
                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
                                  size_t seq_stride);
 size_t attn_tile_smem(int d);
-size_t attn_combine_smem(int S, int d);
 int skinny_gemm(cudaStream_t st, const __half* W, const __half* A, float* Y, int M, int N, int K);
 void transpose_f16(cudaStream_t st, const __half* in, __half* out, int rows, int cols);
 __global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
@@ -1397,8 +1396,7 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
                                                          w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride);
     attn_tile_kernel<<<dim3(B * H, S), 128, attn_tile_smem(d), st>>>(c->bq, kc, vc, B, H, d, c->max_seq, c->bstate,
                                                                      scale_log2, c->bpart, pstep, sstride);
-    attn_combine_kernel<<<B * H, 128, attn_combine_smem(S, d), st>>>(c->bpart, S, B, H, d,
-                                                                      reinterpret_cast<__half*>(c->bctx));
+    attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
     TRY(rgemm(c, st, h, 2 * B, h, sk ? c->bwo[l] : nullptr, w.woT, c->bctx, c->bz));
     TRY(rgemm(c, st, mm, 2 * B, h, w.wup, nullptr, c->ba2, c->bu));
     gelu_hilo_kernel<<<dim3(B, (mm + 255) / 256), 256, 0, st>>>(c->bu, B, mm, w.bup, m.gelu_exact,
@@ -1436,9 +1434,6 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
     const cudaError_t e = cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)attn_tile_smem((int)d));
     if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("attn_tile smem attribute: ") + cudaGetErrorString(e));
-    const cudaError_t e2 = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)attn_combine_smem(c->bsplit, (int)d));
-    if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("combine smem attribute: ") + cudaGetErrorString(e2));
   }
   c->bkc.resize(m.n_layers);
   c->bvc.resize(m.n_layers);

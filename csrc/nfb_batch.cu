@@ -276,8 +276,6 @@ __global__ void attn_combine_kernel(const float* part, int S, int B, int H, int 
   }
 }
 
-size_t attn_combine_smem(int, int) { return 0; }
-
 __device__ __forceinline__ float gelu_f(float x, int exact) {
   if (exact) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
   const float k = 0.79788456080286536f;
