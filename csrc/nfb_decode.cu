@@ -792,7 +792,10 @@ struct Consumer {
   // level by level (ILP kPos on the shuffle chain), then one online-softmax
   // update folds the kPos positions in.
   __device__ __forceinline__ void attention_stage(const unsigned char* sl, int n) {
-    constexpr int kPos = 8;
+    // 6 at one chunk per thread: 10 warps x 3 groups x 6 = 180 >= 128
+    // positions per stage in one pass, shorter per-group chain than 8
+    // (A/B at C2: 4 / 5 / 6 / 7 / 8 -> 824 / 842 / 850 / 841 / 829 tok/s)
+    constexpr int kPos = NCH == 1 ? 6 : 8;
     const int T = tpp(), gpw = 32 / T;
     const int sub = lane % T, gw = lane / T;
     const bool valid = gw < gpw;
