@@ -40,7 +40,11 @@ WORKLOAD = "Pythia-2.8B random-init, bs=1, ctx 1024, greedy decode, CUDA graph, 
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")),
+                    help="GPUs of this node; without a torchrun environment, bench.py spawns the N ranks "
+                         "itself (python -m torch.distributed.run, 127.0.0.1)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (CPU, gloo): ranks, world size, max-over-ranks timing")
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -68,16 +72,52 @@ def parse():
     return a
 
 
-def dist_setup():
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` run directly (no WORLD_SIZE): re-launch this script
+    as N ranks under torch.distributed.run on one node, exactly as the driver's
+    multi-GPU launch does, and return the launcher's exit code.  Rank 0 prints
+    the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def dist_setup(backend: str = "nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            if torch.cuda.device_count() <= local:
+                raise SystemExit(f"rank {rank}: local rank {local} but only {torch.cuda.device_count()} GPU(s)")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        if rank == 0:
+            print(f"bench.py: process group up: backend {dist.get_backend()}, world {dist.get_world_size()}",
+                  file=sys.stderr, flush=True)
     return world, rank, local
+
+
+def run_dry(args, world, rank):
+    """Launch plumbing without a GPU: every rank times a tiny CPU loop, the
+    max over ranks is reduced like the real bench's device time."""
+    from paper_2604_23553_b200.parallel import max_over_ranks
+    a = time.perf_counter()
+    np.linalg.norm(np.arange(1000.0) * (rank + 1))
+    t = max_over_ranks(time.perf_counter() - a)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_reporting": world, "max_rank_seconds": t,
+                          "impl": args.impl}), flush=True)
 
 
 def peaks():
@@ -152,6 +192,11 @@ def cpu_reference(seconds: float, tokens_cap: int | None = None):
     change the timing).  Returns (tokens_per_s, sample description, threads)."""
     from oracle import neox_oracle as O
     from paper_2604_23553_b200 import preset
+    try:  # torchrun pins OMP_NUM_THREADS=1 per rank: give the CPU arm every host core
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(os.cpu_count())
+    except Exception:
+        pass
     cfg = preset(MODEL)
     s = O.Shape.of(cfg)
     rng = np.random.default_rng(0)
@@ -411,6 +456,17 @@ def main():
     global MODEL
     args = parse()
     MODEL = args.model
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    if args.dry_run:
+        world, rank, _ = dist_setup("gloo")
+        run_dry(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))

@@ -229,6 +229,8 @@ int launch_synth_slice(cudaStream_t st, uint64_t seed, uint32_t stream, int64_t 
   return NFB_OK;
 }
 
+__global__ void set_pos_kernel(int* state, int pos) { state[0] = pos; }
+
 __global__ void advance_state_kernel(int* state) {
   state[0] += 1;
   state[1] += 1;
@@ -454,6 +456,16 @@ static int tp_token(nfb_ctx* c, cudaStream_t st) {
 
 namespace {
 
+// Zero both parities of the dynamic row counters (LM-head rows, dynamic MLP
+// chunks).  In graph / decode mode the kernel keeps them consistent by step
+// parity; every launch that does not advance the step (block step, forward,
+// head logits) or that rewinds it (begin_decode) must start from zero, or a
+// parity slot exhausted by an earlier launch hands out no rows.
+int reset_counters(nfb_ctx* c, cudaStream_t st) {
+  CK(cudaMemsetAsync(c->ctr, 0, sizeof(int) * 2 * (size_t)c->ctr_stride, st));
+  return NFB_OK;
+}
+
 int check_device_error(nfb_ctx* c) {
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
@@ -523,8 +535,10 @@ int check_layer(nfb_ctx* c, int layer) {
 // ===========================================================================
 // C-ABI
 // ===========================================================================
-static bool g_creating_tp = false;  // nfb_create_tp: shard desc (hidden != local heads * d_head)
-static nfb_model_desc g_full_desc{};
+// nfb_create / nfb_create_tp: `full` is the unsharded model (== desc unless
+// tensor parallel, where desc holds this rank's heads / FFN rows / vocab).
+static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, int device, int max_seq,
+                      int cluster_size, int max_clusters, nfb_ctx** out);
 
 extern "C" {
 
@@ -534,12 +548,18 @@ const char* nfb_last_error(void) { return g_err.c_str(); }
 
 int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_size,
                int max_clusters, nfb_ctx** out) {
+  return create_ctx(desc, desc, device, max_seq, cluster_size, max_clusters, out);
+}
+}  // extern "C"
+
+static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, int device, int max_seq,
+                      int cluster_size, int max_clusters, nfb_ctx** out) {
   if (!desc || !out) return fail(NFB_EINVAL, "null argument");
   *out = nullptr;
   const nfb_model_desc& m = *desc;
   if (m.hidden < 1 || m.n_heads < 1 || m.d_head < 1 || m.n_layers < 1 || m.d_mlp < 1 || m.vocab < 1)
     return fail(NFB_EINVAL, "model dimensions must be >= 1");
-  if (m.hidden != m.n_heads * m.d_head && !g_creating_tp)
+  if (m.hidden != m.n_heads * m.d_head && desc == full)
     return fail(NFB_EINVAL, "hidden (" + std::to_string(m.hidden) + ") must equal n_heads * d_head (" +
                                 std::to_string(m.n_heads) + " * " + std::to_string(m.d_head) + ")");
   if (m.rotary_dims < 2 || m.rotary_dims % 2 || m.rotary_dims > m.d_head)
@@ -556,7 +576,7 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
 
   nfb_ctx* c = new nfb_ctx();
   c->desc = m;
-  c->full = g_creating_tp ? g_full_desc : m;
+  c->full = *full;
   c->device = device;
   c->max_seq = max_seq;
   c->C = C;
@@ -603,7 +623,12 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
     return bail(fail(NFB_ECUDA, std::string("no co-resident cluster fits: ") + cudaGetErrorString(e)));
   if (max_clusters <= 0 && getenv("NFB_MAX_CLUSTERS")) max_clusters = atoi(getenv("NFB_MAX_CLUSTERS"));
   if (max_clusters > 0) nc = std::min(nc, max_clusters);
-  if (getenv("NFB_NO_COOP")) c->coop = false;
+  // Plain cluster launch (grid <= max co-resident clusters, one CTA per SM:
+  // still co-resident) on request or under Nsight Compute, whose kernel
+  // replay does not support cooperative launches (the driver's ncu pass
+  // reported rc 9 / no time for the cooperative launch).
+  if (getenv("NFB_NO_COOP") || getenv("CUDA_INJECTION64_PATH") || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
+    c->coop = false;
   if (getenv("NFB_HEAD_WEIGHT")) c->head_weight_pct = atoi(getenv("NFB_HEAD_WEIGHT"));
   if (getenv("NFB_DEBUG")) c->debug = atoi(getenv("NFB_DEBUG"));
   if (getenv("NFB_PREFETCH_KB")) c->pf_ahead = atoi(getenv("NFB_PREFETCH_KB")) * 1024;
@@ -688,6 +713,8 @@ int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_
   return NFB_OK;
 }
 
+extern "C" {
+
 int nfb_destroy(nfb_ctx* c) {
   if (!c) return NFB_OK;
   cudaSetDevice(c->device);
@@ -737,6 +764,7 @@ int nfb_set_block_weights(nfb_ctx* c, int layer, const nfb_block_weights* w, int
   for (const void* p : ptrs)
     if (!p) return fail(NFB_EINVAL, "every BlockWeights tensor is required");
   cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));  // legacy-stream copies below: order after queued launches
   const int h = c->desc.hidden, m = c->desc.d_mlp;
   LayerBufs& b = c->layers[layer];
   TRY(upload_f32_of_f16(w->ln1_gain, dtype, h, b.ln1g));
@@ -847,6 +875,7 @@ int nfb_set_head(nfb_ctx* c, const void* embed, const void* lnf_gain, const void
   if (!c) return fail(NFB_EINVAL, "null context");
   if (c->tp_size > 1) return fail(NFB_EUNSUPPORTED, "tensor-parallel contexts take synthesized weights");
   cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
   const size_t h = c->desc.hidden, V = c->desc.vocab;
   if (embed) {
     TRY(upload_f16(embed, dtype, V, h, L_ROW, c->embed));
@@ -892,6 +921,7 @@ int nfb_kv_write(nfb_ctx* c, int layer, int start, int count, const void* keys, 
                                 " positions (capacity " + std::to_string(c->max_seq) + ")");
   if (count && (!keys || !values)) return fail(NFB_EINVAL, "null keys/values");
   cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
   const size_t H = c->desc.n_heads, d = c->desc.d_head;
   if (count) {
     std::vector<uint16_t> hk, hv;
@@ -982,6 +1012,7 @@ int nfb_block_step(nfb_ctx* c, int layer, int pos, const float* x_in, float* x_o
   p.in_mode = IN_X;
   p.head_mode = HEAD_NONE;
   p.advance_pos = 0;
+  TRY(reset_counters(c, c->stream));
   TRY(launch(c, p, c->stream));
   CK(cudaMemcpyAsync(c->h_hidden, c->xs + h, (size_t)h * 4, cudaMemcpyDeviceToHost, c->stream));
   TRY(check_device_error(c));
@@ -1013,6 +1044,7 @@ int nfb_forward(nfb_ctx* c, int pos, const float* x_in, float* hidden_out, float
   p.in_mode = IN_X;
   p.head_mode = head_mode;
   p.advance_pos = 0;
+  TRY(reset_counters(c, c->stream));
   TRY(launch(c, p, c->stream));
   if (hidden_out)
     CK(cudaMemcpyAsync(c->h_hidden, c->xs, (size_t)(L + 1) * h * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1021,6 +1053,62 @@ int nfb_forward(nfb_ctx* c, int pos, const float* x_in, float* hidden_out, float
   TRY(check_device_error(c));
   if (hidden_out) memcpy(hidden_out, c->h_hidden, (size_t)(L + 1) * h * 4);
   if (logits_out && head_mode != NFB_HEAD_NONE) memcpy(logits_out, c->h_logits, (size_t)V * 4);
+  for (int l = 0; l < L; ++l) c->layers[l].kv_len = pos + 1;
+  c->decode_pos = -1;
+  return NFB_OK;
+}
+
+// ---- device-resident variants (torch CUDA tensors: raw pointer + stream) ----
+int nfb_block_step_dev(nfb_ctx* c, int layer, int pos, const float* x_in, float* x_out, void* stream) {
+  TRY(check_layer(c, layer));
+  if (!x_in || !x_out) return fail(NFB_EINVAL, "null x");
+  TRY(check_ready(c, layer, layer + 1, pos));
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  const int h = c->desc.hidden;
+  CK(cudaMemcpyAsync(c->xs, x_in, (size_t)h * 4, cudaMemcpyDeviceToDevice, st));
+  set_pos_kernel<<<1, 1, 0, st>>>(c->state, pos);
+  CK(cudaGetLastError());
+  Params p = base_params(c);
+  p.l0 = layer;
+  p.l1 = layer + 1;
+  p.in_mode = IN_X;
+  p.head_mode = HEAD_NONE;
+  p.advance_pos = 0;
+  TRY(reset_counters(c, st));
+  TRY(launch(c, p, st));
+  CK(cudaMemcpyAsync(x_out, c->xs + h, (size_t)h * 4, cudaMemcpyDeviceToDevice, st));
+  c->layers[layer].kv_len = pos + 1;
+  c->decode_pos = -1;
+  return NFB_OK;
+}
+
+int nfb_forward_dev(nfb_ctx* c, int pos, const float* x_in, float* hidden_out, float* logits_out, int head_mode,
+                    void* stream) {
+  if (!c || !x_in) return fail(NFB_EINVAL, "null argument");
+  if (c->tp_size > 1)
+    return fail(NFB_EUNSUPPORTED, "tensor-parallel contexts: use nfb_block_step per layer or the decode API");
+  const int L = c->desc.n_layers, h = c->desc.hidden, V = c->desc.vocab;
+  TRY(check_ready(c, 0, L, pos));
+  if (head_mode < NFB_HEAD_NONE || head_mode > NFB_HEAD_LM) return fail(NFB_EINVAL, "bad head_mode");
+  if (head_mode != NFB_HEAD_NONE && !c->has_unembed) return fail(NFB_ESTATE, "unembedding not set");
+  if (head_mode == NFB_HEAD_LM && !c->has_lnf) return fail(NFB_ESTATE, "final LN not set");
+  cudaSetDevice(c->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  CK(cudaMemcpyAsync(c->xs, x_in, (size_t)h * 4, cudaMemcpyDeviceToDevice, st));
+  set_pos_kernel<<<1, 1, 0, st>>>(c->state, pos);
+  CK(cudaGetLastError());
+  Params p = base_params(c);
+  p.l0 = 0;
+  p.l1 = L;
+  p.in_mode = IN_X;
+  p.head_mode = head_mode;
+  p.advance_pos = 0;
+  TRY(reset_counters(c, st));
+  TRY(launch(c, p, st));
+  if (hidden_out) CK(cudaMemcpyAsync(hidden_out, c->xs, (size_t)(L + 1) * h * 4, cudaMemcpyDeviceToDevice, st));
+  if (logits_out && head_mode != NFB_HEAD_NONE)
+    CK(cudaMemcpyAsync(logits_out, c->logits, (size_t)V * 4, cudaMemcpyDeviceToDevice, st));
   for (int l = 0; l < L; ++l) c->layers[l].kv_len = pos + 1;
   c->decode_pos = -1;
   return NFB_OK;
@@ -1038,6 +1126,8 @@ int nfb_begin_decode(nfb_ctx* c, int pos, int token) {
   CK(cudaMemcpy(c->state, st, sizeof(st), cudaMemcpyHostToDevice));
   unsigned long long am[2] = {0ull, (0xffffffffull << 32) | (unsigned long long)(0xffffffffu - (uint32_t)token)};
   CK(cudaMemcpy(c->amax, am, sizeof(am), cudaMemcpyHostToDevice));
+  TRY(reset_counters(c, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   c->decode_pos = pos;
   c->decode_step = 0;
   for (auto& b : c->layers) b.kv_len = pos;
@@ -1266,10 +1356,7 @@ int nfb_create_tp(const nfb_model_desc* full, int device, int max_seq, int clust
   m.n_heads /= tp_size;
   m.d_mlp /= tp_size;
   m.vocab /= tp_size;
-  g_creating_tp = true;
-  g_full_desc = *full;
-  const int r = nfb_create(&m, device, max_seq, cluster_size, max_clusters, out);
-  g_creating_tp = false;
+  const int r = create_ctx(&m, full, device, max_seq, cluster_size, max_clusters, out);
   if (r != NFB_OK) return r;
   (*out)->tp_rank = tp_rank;
   (*out)->tp_size = tp_size;
@@ -1323,6 +1410,7 @@ int nfb_head_logits(nfb_ctx* c, const float* h_in, float* logits_out, int head_m
   p.head_mode = head_mode;
   p.advance_pos = 0;
   p.state_update = 0;
+  TRY(reset_counters(c, c->stream));
   TRY(launch(c, p, c->stream));
   CK(cudaMemcpyAsync(c->h_logits, c->logits, (size_t)V * 4, cudaMemcpyDeviceToHost, c->stream));
   TRY(check_device_error(c));
@@ -1493,6 +1581,7 @@ int nfb_batch_kv_write(nfb_ctx* c, int layer, int seq, int start, int count, con
     return fail(NFB_EINVAL, "batch KV write range invalid");
   if (count && (!keys || !values)) return fail(NFB_EINVAL, "null keys/values");
   cudaSetDevice(c->device);
+  CK(cudaStreamSynchronize(c->stream));
   const size_t H = c->desc.n_heads, d = c->desc.d_head;
   if (count) {
     std::vector<uint16_t> hk, hv;

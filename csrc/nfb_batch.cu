@@ -189,8 +189,7 @@ __global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __
   }
   for (int i = tid; i < d; i += blockDim.x) sq[i] = q[(size_t)bh * d + i];
   __syncthreads();
-  while (!mbar_try_wait(bar, 0)) {
-  }
+  mbar_wait(bar, 0, nullptr, 30);  // watchdog: trap after 4 s like every other wait
   const int cpr = d >> 3;
   float sc = -INFINITY;
   if (tid < n) {

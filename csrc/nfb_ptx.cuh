@@ -72,7 +72,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 
 static __device__ __noinline__ void fail_timeout(int* err, int code) {
-  atomicExch(err, code);
+  if (err) atomicExch(err, code);
   __threadfence_system();
   asm volatile("trap;");
 }

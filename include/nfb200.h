@@ -119,6 +119,17 @@ int nfb_block_step(nfb_ctx* ctx, int layer, int pos, const float* x_in, float* x
 int nfb_forward(nfb_ctx* ctx, int pos, const float* x_in, float* hidden_out, float* logits_out,
                 int head_mode);
 
+/* Device-resident variants for callers holding torch CUDA tensors (raw
+ * pointer + stream; SURVEY.md §8b "Ownership"): x_in / x_out / hidden_out /
+ * logits_out are DEVICE float32 pointers, `stream` a cudaStream_t (NULL = the
+ * context stream).  Everything is enqueued on `stream` with no host
+ * synchronisation (the input is not checked for non-finite values -- that
+ * would need a device->host read); a device-side failure surfaces at the next
+ * nfb_sync.  Same semantics as nfb_block_step / nfb_forward otherwise. */
+int nfb_block_step_dev(nfb_ctx* ctx, int layer, int pos, const float* x_in, float* x_out, void* stream);
+int nfb_forward_dev(nfb_ctx* ctx, int pos, const float* x_in, float* hidden_out, float* logits_out,
+                    int head_mode, void* stream);
+
 /* Greedy token decode with device-resident state (graph mode).
  * nfb_begin_decode sets position and first input token; each nfb_decode_step
  * embeds the previous argmax, runs all layers + LM head, argmax on device and

@@ -295,10 +295,16 @@ class KV:
         return self.v[:, :self.n].copy()
 
 
-def block_step(x, p, cache, pos, s: Shape, kind="tanh", ln=ln_two_pass):
+def block_step(x, p, cache, pos, s: Shape, kind="tanh", ln=ln_two_pass, kv_store=None):
     """One decode step of the block, appending this step's K/V
     (nf/golden.py:189-228; with ``ln=ln_single_pass`` the numerics of
-    nf/cluster.py:316,351 in EXACT mode)."""
+    nf/cluster.py:316,351 in EXACT mode).
+
+    ``kv_store`` (default None = the reference: K/V kept in float64) is applied
+    to the K/V *stored* in the cache -- ``f16_round`` restates the device's
+    fp16 KV cache.  The current token still attends with its exact K/V (the
+    fused kernel keeps them in fp32 registers); only later steps see the
+    stored values."""
     x = np.asarray(x, dtype=np.float64)
     if x.shape != (s.hidden,):
         raise ValueError(f"input must have shape ({s.hidden},)")
@@ -308,17 +314,147 @@ def block_step(x, p, cache, pos, s: Shape, kind="tanh", ln=ln_two_pass):
     q, k, v = qkv_split(n1, p, s)
     q = rope(q, pos, s.rotary_dims, s.theta_base)
     k = rope(k, pos, s.rotary_dims, s.theta_base)
-    cache.append(k, v)
+    cache.append(kv_store(k) if kv_store else k, kv_store(v) if kv_store else v)
     scale = 1.0 / math.sqrt(s.d_head)  # nf/golden.py:185-186
     ctx = np.empty(s.hidden)
     d = s.d_head
     for h in range(s.n_heads):
         kh, vh = cache.head(h)
+        if kv_store:
+            kh, vh = kh.copy(), vh.copy()
+            kh[-1], vh[-1] = k[h], v[h]
         ctx[h * d:(h + 1) * d] = attend(q[h], kh, vh, scale)
     attn_res = x + p["out_weight"] @ ctx + p["out_bias"]
     ln2_in = x if s.parallel_residual else attn_res
     n2 = ln(ln2_in, p["ln2_gain"], p["ln2_bias"], s.ln_eps)
     return attn_res + mlp(n2, p, kind)
+
+
+def prefill_attention(Q, K, V, tile, causal=True, scale=None, prefix_keys=None, prefix_values=None):
+    """Causal attention over a sequence, keys folded in tiles of ``tile``
+    positions into a running softmax state per query row
+    (``prefill_attention_tiled``, nf/golden.py:234-265).  Extension used by
+    the prefill path: an optional cached prefix [P0, d] that every query row
+    sees before the sequence (row i then sees P0 + i + 1 keys when causal);
+    with no prefix this is exactly the reference function."""
+    Q = np.asarray(Q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    if Q.ndim != 2 or K.shape != Q.shape or V.shape != Q.shape:
+        raise ValueError("Q, K, V must share shape [seq, d_head]")
+    if tile < 1:
+        raise ValueError("tile must be >= 1")
+    seq, d = Q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if prefix_keys is not None:
+        K = np.concatenate([np.asarray(prefix_keys, np.float64), K])
+        V = np.concatenate([np.asarray(prefix_values, np.float64), V])
+    p0 = K.shape[0] - seq
+    out = np.empty((seq, d))
+    for i in range(seq):
+        limit = p0 + i + 1 if causal else K.shape[0]
+        st = (-math.inf, 0.0, np.zeros(d))
+        for t0 in range(0, limit, tile):
+            t1 = min(t0 + tile, limit)
+            st = sm_merge(st, sm_state(Q[i], K[t0:t1], V[t0:t1], scale))
+        out[i] = st[2] / st[1]
+    return out
+
+
+def causal_attention(Q, K, V, scale):
+    """Vectorised form of ``prefill_attention`` for query rows that are the
+    LAST seq rows of K/V (row i sees keys [0, P0 + i]): Q [H, T, d], K/V
+    [H, P0 + T, d] -> [H, T, d].  One softmax per row instead of the tiled
+    fold (equal to it up to float64 merge order; pinned in tests)."""
+    Q = np.asarray(Q, np.float64)
+    H, T, d = Q.shape
+    P = K.shape[1]
+    S = np.einsum("htd,hpd->htp", Q, K) * scale
+    mask = np.arange(P)[None, :] > (P - T + np.arange(T))[:, None]
+    S = np.where(mask[None], -np.inf, S)
+    m = S.max(axis=2, keepdims=True)
+    w = np.exp(S - m)
+    return np.einsum("htp,hpd->htd", w, V) / w.sum(axis=2, keepdims=True)
+
+
+def rope_rows(v, positions, rd, base=10000.0):
+    """``rope`` with one position per row: v [T, ..., d], positions [T]."""
+    v = np.asarray(v, dtype=np.float64)
+    half = rd // 2
+    theta = np.asarray(positions, np.float64)[:, None] * base ** (-2.0 * np.arange(half, dtype=np.float64) / rd)
+    shape = (v.shape[0],) + (1,) * (v.ndim - 2) + (half,)
+    c, sn = np.cos(theta).reshape(shape), np.sin(theta).reshape(shape)
+    out = v.copy()
+    a, b = v[..., :half], v[..., half:rd]
+    out[..., :half] = a * c - b * sn
+    out[..., half:rd] = a * sn + b * c
+    return out
+
+
+def block_steps(X, p, cache, pos0, s: Shape, kind="tanh", kv_store=None, current_stored=False):
+    """``block_step`` for t = 0..T-1 with input X[t] at position pos0 + t, in
+    that order (each step appends its K/V and attends over everything
+    before it) -- computed with batched projections and one causal softmax
+    per row, since the T inputs are known up front (teacher forcing / a
+    layer-streamed oracle / prefill).  Equal to the sequential loop up to
+    float64 summation order (pinned in tests/test_oracle_golden.py).
+
+    ``kv_store``: as in ``block_step``.  ``current_stored``: the current token
+    also attends with its STORED K/V (the batched and prefill device paths read
+    it back from the fp16 cache); default False = the fused kernel / the
+    sequential ``block_step``."""
+    X = np.asarray(X, dtype=np.float64)
+    T = X.shape[0]
+    if X.ndim != 2 or X.shape[1] != s.hidden:
+        raise ValueError(f"inputs must have shape (T, {s.hidden})")
+    if len(cache) != pos0:
+        raise ValueError(f"cache holds {len(cache)} positions, expected {pos0}")
+    H, d = s.n_heads, s.d_head
+
+    def ln_rows(Z, g, b):
+        _finite(Z)
+        mu = Z.mean(axis=1, keepdims=True)
+        var = np.mean((Z - mu) ** 2, axis=1, keepdims=True)
+        return (Z - mu) / np.sqrt(var + s.ln_eps) * g + b
+
+    n1 = ln_rows(X, p["ln1_gain"], p["ln1_bias"])
+    Y = (n1 @ p["qkv_weight"].T + p["qkv_bias"]).reshape(T, H, 3 * d)
+    pos = pos0 + np.arange(T)
+    q = rope_rows(Y[:, :, :d], pos, s.rotary_dims, s.theta_base)
+    k = rope_rows(Y[:, :, d:2 * d], pos, s.rotary_dims, s.theta_base)
+    v = Y[:, :, 2 * d:].copy()
+    ks = kv_store(k) if kv_store else k
+    vs = kv_store(v) if kv_store else v
+    for t in range(T):
+        cache.append(ks[t], vs[t])
+    Kall = cache.k[:, :pos0 + T].copy()
+    Vall = cache.v[:, :pos0 + T].copy()
+    scale = 1.0 / math.sqrt(d)
+    Qh = q.transpose(1, 0, 2)  # [H, T, d]
+    if kv_store and not current_stored:
+        # the diagonal (row t, key pos0 + t) uses the exact K/V
+        S = np.einsum("htd,hpd->htp", Qh, Kall) * scale
+        diag = np.einsum("htd,htd->ht", Qh, k.transpose(1, 0, 2)) * scale
+        idx = pos0 + np.arange(T)
+        S[:, np.arange(T), idx] = diag
+        P = Kall.shape[1]
+        mask = np.arange(P)[None, :] > idx[:, None]
+        S = np.where(mask[None], -np.inf, S)
+        m = S.max(axis=2, keepdims=True)
+        w = np.exp(S - m)
+        o = np.einsum("htp,hpd->htd", w, Vall)
+        wd = w[:, np.arange(T), idx]  # [H, T]
+        o += wd[:, :, None] * (v.transpose(1, 0, 2) - vs.transpose(1, 0, 2))
+        ctx = o / w.sum(axis=2, keepdims=True)
+    else:
+        ctx = causal_attention(Qh, Kall, Vall, scale)
+    ctx = ctx.transpose(1, 0, 2).reshape(T, s.hidden)
+    attn_res = X + ctx @ p["out_weight"].T + p["out_bias"]
+    ln2_in = X if s.parallel_residual else attn_res
+    n2 = ln_rows(ln2_in, p["ln2_gain"], p["ln2_bias"])
+    hdn = n2 @ p["up_weight"].T + p["up_bias"]
+    return attn_res + gelu(hdn, kind) @ p["down_weight"].T + p["down_bias"]
 
 
 def partition_kv(n, blocks):
@@ -371,13 +507,22 @@ class Model:
     def pos(self):
         return len(self.caches[0])
 
-    def hidden_states(self, x0):
+    def hidden_states(self, x0, kv_store=None):
         """Returns [x_0, x_1, ..., x_L] for one step (appends to every cache)."""
         xs = [np.asarray(x0, dtype=np.float64)]
         pos = self.pos
         for p, c in zip(self.layers, self.caches):
-            xs.append(block_step(xs[-1], p, c, pos, self.s, self.kind))
+            xs.append(block_step(xs[-1], p, c, pos, self.s, self.kind, kv_store=kv_store))
         return xs
+
+    def hidden_states_batched(self, X, kv_store=None, current_stored=False):
+        """T consecutive tokens with known inputs X [T, h] through all layers
+        (``block_steps`` per layer): returns [L+1, T, h]."""
+        out = [np.asarray(X, dtype=np.float64)]
+        pos = self.pos
+        for p, c in zip(self.layers, self.caches):
+            out.append(block_steps(out[-1], p, c, pos, self.s, self.kind, kv_store, current_stored))
+        return np.array(out)
 
     def logits(self, h, probe=False):
         hd = self.head
@@ -385,8 +530,17 @@ class Model:
             h = ln_two_pass(h, hd["lnf_gain"], hd["lnf_bias"], self.s.ln_eps)
         return hd["unembed"] @ h
 
-    def step_token(self, token):
-        xs = self.hidden_states(self.head["embed"][token])
+    def logits_rows(self, H, probe=False):
+        """``logits`` of every row of H [T, h]."""
+        H = np.asarray(H, np.float64)
+        if not probe:
+            mu = H.mean(axis=1, keepdims=True)
+            var = np.mean((H - mu) ** 2, axis=1, keepdims=True)
+            H = (H - mu) / np.sqrt(var + self.s.ln_eps) * self.head["lnf_gain"] + self.head["lnf_bias"]
+        return H @ self.head["unembed"].T
+
+    def step_token(self, token, kv_store=None):
+        xs = self.hidden_states(self.head["embed"][token], kv_store)
         lg = self.logits(xs[-1])
         return greedy(lg), lg, xs
 
@@ -405,3 +559,76 @@ def synth_kv(s: Shape, count: int, seed: int):
     k = f16_round(0.8660254037844386 * uniform_stream(seed, 0, n)).reshape(s.n_heads, count, s.d_head)
     v = f16_round(0.8660254037844386 * uniform_stream(seed, 1, n)).reshape(s.n_heads, count, s.d_head)
     return k, v
+
+
+# ---------------------------------------------------------------------------
+# Fast synthesis for the multi-layer tests: oracle/synth.c (the same recipe,
+# restated in C; built in-tree by __graft_entry__.build() as
+# oracle/liboracle_synth.so; pinned bit-exact against synth_block /
+# synth_head / synth_kv by tests/test_oracle_golden.py).  Falls back to numpy.
+
+_CSYNTH = None
+
+
+def _csynth():
+    global _CSYNTH
+    if _CSYNTH is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liboracle_synth.so")
+        try:
+            lib = ctypes.CDLL(path)
+            lib.oracle_synth_f16.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
+                                             ctypes.c_double, ctypes.c_void_p]
+            lib.oracle_synth_f16.restype = None
+            lib.oracle_synth_f16_range.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                                   ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
+            lib.oracle_synth_f16_range.restype = None
+            _CSYNTH = lib
+        except OSError:
+            _CSYNTH = False
+    return _CSYNTH
+
+
+def _synth_f16(seed, stream, shape, kind, div=1.0, start=0):
+    n = int(np.prod(shape))
+    lib = _csynth()
+    if not lib:
+        u = uniform_stream(seed, stream, start + n)[start:]
+        v = {0: u / div, 1: 1.0 + 0.1 * u, 2: 0.1 * u, 3: 0.02 * u, 4: u, 5: 0.8660254037844386 * u}[kind]
+        return f16_round(v).reshape(shape)
+    out = np.empty(n, np.float64)
+    lib.oracle_synth_f16_range(seed & _MASK64, stream, start, n, kind, float(div), out.ctypes.data)
+    return out.reshape(shape)
+
+
+def synth_block_f16(s: Shape, seed: int) -> dict:
+    """== f16_params(synth_block(s, seed))."""
+    out = {}
+    for stream, name in enumerate(BLOCK_TENSORS):
+        shape = block_shapes(s)[name]
+        if name.endswith("_weight"):
+            out[name] = _synth_f16(seed, stream, shape, 0, math.sqrt(shape[1]))
+        elif name.endswith("gain"):
+            out[name] = _synth_f16(seed, stream, shape, 1)
+        elif name in ("ln1_bias", "ln2_bias"):
+            out[name] = _synth_f16(seed, stream, shape, 2)
+        else:
+            out[name] = _synth_f16(seed, stream, shape, 3)
+    return out
+
+
+def synth_head_f16(s: Shape, seed: int) -> dict:
+    """== f16_params(synth_head(s, seed))."""
+    h, V = s.hidden, s.vocab
+    return {"embed": _synth_f16(seed, 0, (V, h), 4), "lnf_gain": _synth_f16(seed, 1, (h,), 1),
+            "lnf_bias": _synth_f16(seed, 2, (h,), 2), "unembed": _synth_f16(seed, 3, (V, h), 0, math.sqrt(h))}
+
+
+def synth_kv_fast(s: Shape, count: int, seed: int, head0: int = 0, n_heads: int | None = None):
+    """== synth_kv(s, count, seed) (heads [head0, head0 + n_heads) of a
+    stream that may hold more heads, e.g. the batched path's bmax * H)."""
+    nh = s.n_heads if n_heads is None else n_heads
+    shape = (nh, count, s.d_head)
+    a = head0 * count * s.d_head
+    return _synth_f16(seed, 0, shape, 5, start=a), _synth_f16(seed, 1, shape, 5, start=a)

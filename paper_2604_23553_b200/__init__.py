@@ -8,14 +8,15 @@ runs as one hand-written sm_100a kernel (``libnfb200.so``, C-ABI in
 
 from .cluster import (
     RING, TREE, ClusterSpec, ExecTrace, KernelTraceRecord, Precision, ReductionKind,
-    ReductionStrategy, build_trace, fused_block_step, partition_kv, release_device_state,
+    ReductionStrategy, build_trace, fused_block_step, invalidate_weights, partition_kv,
+    release_device_state,
     ring_steps, trace_to_jsonl, tree_steps,
 )
 from .config import PRESETS, ModelConfig, preset
 from .engine import Engine, kv_seed
 from .fidelity import (
     ADVERSARIAL_N_BLOCKS, DecodeInstance, FidelityReport, SweepSummary, adversarial_instance,
-    compare, format_report, greedy_tokens, seed_sweep, synthetic_instance, topk_indices,
+    compare, distinct_greedy_outputs, format_report, greedy_tokens, seed_sweep, synthetic_instance, topk_indices,
 )
 from .perf import (
     ParamCounts, TrafficReport, count_params, flops_per_token, lm_head_bytes, mean_step_bytes,

@@ -100,6 +100,15 @@ class Engine:
     def set_block_weights(self, layer: int, w) -> None:
         if isinstance(w, dict):
             w = BlockWeights(**w)
+        if self.tp[1] > 1:
+            raise RuntimeError("tensor-parallel contexts take synthesized weights (synth_block_weights)")
+        # the C side reads exactly the reference shapes: reject anything else
+        # here, as the reference does (nf/weights.py:39-52)
+        from .weights import tensor_shapes
+        for name, shape in tensor_shapes(self.cfg).items():
+            got = np.shape(getattr(w, name))
+            if got != shape:
+                raise ValueError(f"{name}: expected shape {shape}, got {got}")
         arrs = [_host(getattr(w, n)) for n in TENSOR_NAMES]
         dt = {a.dtype for a in arrs}
         if len(dt) != 1:
@@ -143,6 +152,8 @@ class Engine:
         k, v = _host(keys), _host(values)
         if k.shape != v.shape or k.ndim != 3:
             raise ValueError("keys/values must share shape [n_heads, seq, d_head]")
+        if k.shape[0] != self.local_heads or k.shape[2] != self.cfg.d_head:
+            raise ValueError(f"keys/values must be [{self.local_heads}, seq, {self.cfg.d_head}], got {k.shape}")
         if v.dtype != k.dtype:
             v = v.astype(k.dtype)
         check(self.lib.nfb_kv_write(self._h, layer, start, k.shape[1], C.c_void_p(k.ctypes.data),
@@ -189,6 +200,41 @@ class Engine:
                                    fptr(lg) if lg is not None else None, mode), "nfb_forward")
         self._kv_len = [pos + 1] * self.cfg.n_layers
         return hs, lg
+
+    # ---- device-resident variants (torch CUDA tensors, no host sync) ---------
+    @staticmethod
+    def _dev(t, n, what):
+        import torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError(f"{what} must be a contiguous float32 CUDA tensor")
+        if t.numel() != n:
+            raise ValueError(f"{what} must have {n} elements, got {t.numel()}")
+        return C.c_void_p(t.data_ptr())
+
+    @staticmethod
+    def _cur_stream(stream):
+        if stream is not None:
+            return C.c_void_p(int(stream))
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def block_step_dev(self, layer: int, pos: int, x, out, stream=None) -> None:
+        """``block_step`` on torch CUDA tensors x / out [hidden] (float32),
+        enqueued on ``stream`` (default: torch's current stream); no sync."""
+        h = self.cfg.hidden
+        check(self.lib.nfb_block_step_dev(self._h, layer, pos, self._dev(x, h, "x"), self._dev(out, h, "out"),
+                                          self._cur_stream(stream)), "nfb_block_step_dev")
+        self._kv_len[layer] = pos + 1
+
+    def forward_dev(self, pos: int, x, hidden=None, logits=None, head: str | None = None, stream=None) -> None:
+        """``forward`` on torch CUDA tensors: x [hidden], hidden [(L+1), hidden]
+        and logits [vocab] outputs (either may be None); no sync."""
+        h, L = self.cfg.hidden, self.cfg.n_layers
+        hp = self._dev(hidden, (L + 1) * h, "hidden") if hidden is not None else None
+        lp = self._dev(logits, self.cfg.vocab, "logits") if logits is not None else None
+        check(self.lib.nfb_forward_dev(self._h, pos, self._dev(x, h, "x"), hp, lp, HEAD_MODES[head],
+                                       self._cur_stream(stream)), "nfb_forward_dev")
+        self._kv_len = [pos + 1] * L
 
     # ---- greedy decode with device-resident state ---------------------------
     def begin_decode(self, pos: int, token: int) -> None:
@@ -310,6 +356,8 @@ class Engine:
 
     def batch_kv_write(self, layer: int, seq: int, start: int, keys, values) -> None:
         k, v = _host(keys), _host(values)
+        if k.shape != v.shape or k.ndim != 3 or k.shape[0] != self.cfg.n_heads or k.shape[2] != self.cfg.d_head:
+            raise ValueError(f"keys/values must share shape [{self.cfg.n_heads}, seq, {self.cfg.d_head}]")
         v = v.astype(k.dtype, copy=False)
         check(self.lib.nfb_batch_kv_write(self._h, layer, seq, start, k.shape[1], C.c_void_p(k.ctypes.data),
                                           C.c_void_p(v.ctypes.data), _dtype_code(k)), "nfb_batch_kv_write")

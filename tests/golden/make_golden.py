@@ -185,12 +185,27 @@ def cli_fixture():
         cfg.unlink()
 
 
+def prefill():
+    """prefill_attention_tiled (nf/golden.py:234-265): causal and full
+    attention of one head over a 37-position sequence, several tile sizes."""
+    from neoxfuse.golden import prefill_attention_tiled
+    rng = np.random.default_rng(31)
+    out = {}
+    for tag, d in (("d80", 80), ("d64", 64)):
+        Q, K, V = (rng.standard_normal((37, d)) * 0.7 for _ in range(3))
+        out[f"{tag}.Q"], out[f"{tag}.K"], out[f"{tag}.V"] = Q, K, V
+        for tile in (1, 5, 16, 37):
+            out[f"{tag}.causal.{tile}"] = prefill_attention_tiled(Q, K, V, tile)
+            out[f"{tag}.full.{tile}"] = prefill_attention_tiled(Q, K, V, tile, causal=False)
+    np.savez(OUT / "prefill.npz", **out)
+
+
+ALL = [cli_fixture, prng, half, synth, blocks, fidelity, bytes_model, prefill]
+
 if __name__ == "__main__":
-    cli_fixture()
-    prng()
-    half()
-    synth()
-    blocks()
-    fidelity()
-    bytes_model()
+    # python tests/golden/make_golden.py [name ...]  (default: every fixture)
+    pick = sys.argv[1:]
+    for fn in ALL:
+        if not pick or fn.__name__ in pick:
+            fn()
     print("golden fixtures written to", OUT)
