@@ -3,7 +3,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
-#include <cublas_v2.h>
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -31,7 +31,13 @@ __global__ void attn_tile_kernel(const float* q, const __half* kc, const __half*
                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
                                  size_t seq_stride);
 size_t attn_tile_smem(int d);
-int skinny_gemm(cudaStream_t st, const __half* W, const __half* A, float* Y, int M, int N, int K);
+// tcgen05 GEMM (csrc/nfb_umma.cu)
+int make_tmap_f16(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows, uint64_t ld, int box_rows);
+bool umma_encoder_available();
+int umma_n_pad(int N);
+void umma_plan(int M, int N, int K, int sm_count, int* grid, int* max_pieces);
+cudaError_t umma_gemm(cudaStream_t st, const CUtensorMap* tw, const CUtensorMap* ta, int M, int N, int K, float* Y,
+                      float* ws, int* counters, int* err, int sm_count);
 void transpose_f16(cudaStream_t st, const __half* in, __half* out, int rows, int cols);
 __global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
 __global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
@@ -283,10 +289,11 @@ struct nfb_ctx {
   int tp_rank = 0, tp_size = 1;
   nfb_model_desc full{};  // the unsharded model (desc holds this rank's shard)
   void* nccl = nullptr;   // ncclComm_t
-  // batched decode (nfb_batch_*): B sequences at one position, cuBLAS GEMMs
+  // batched decode (nfb_batch_*): B sequences at one position, tcgen05 GEMMs
   int bmax = 0, bcur = 0, bsplit = 1;
-  // skinny-GEMM layouts of W_out / W_down ([h][h], [h][d_mlp] row-major) for
-  // batches of <= 4 sequences, rebuilt when the weights change (wver)
+  // row-major W_out / W_down ([h][h], [h][d_mlp]: K-major UMMA operands),
+  // rebuilt from the decode kernel's transposed copies when the weights
+  // change (wver)
   std::vector<uint16_t*> bwo, bwd;
   unsigned long long wver = 1, bt_ver = 0;
   std::vector<uint16_t*> bkc, bvc;  // per layer [bmax][H][max_seq][d]
@@ -295,8 +302,16 @@ struct nfb_ctx {
   uint16_t *ba1 = nullptr, *ba2 = nullptr, *bctx = nullptr, *bg = nullptr;
   int *btok = nullptr, *bstate = nullptr;
   int bpos = -1;
-  void* cublas = nullptr;  // cublasHandle_t
-  void* cublas_ws = nullptr;
+  // TMA tensor maps: per layer [qkv, out, up, down] weights, the LM head, and
+  // the activation operands for the current batch (rebuilt when it changes)
+  std::vector<CUtensorMap> bmap_w;  // [layer * 4 + j]
+  CUtensorMap bmap_lm{};
+  CUtensorMap bmap_a1{}, bmap_a2{}, bmap_ctx{}, bmap_g{};
+  int bmap_rows = 0;                 // batch the activation maps were built for
+  float* uws = nullptr;              // stream-K partials
+  int* uctr = nullptr;               // stream-K tile counters
+  size_t uws_floats = 0;
+  int uctr_n = 0;
   cudaGraph_t bgraph = nullptr;
   cudaGraphExec_t bgexec = nullptr;
   unsigned long long* gbar = nullptr;
@@ -722,7 +737,6 @@ int nfb_destroy(nfb_ctx* c) {
   if (c->nccl && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)c->nccl);
   if (c->bgexec) cudaGraphExecDestroy(c->bgexec);
   if (c->bgraph) cudaGraphDestroy(c->bgraph);
-  if (c->cublas) cublasDestroy((cublasHandle_t)c->cublas);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   for (void* p : c->allocs) cudaFree(p);
@@ -1422,37 +1436,45 @@ int nfb_head_logits(nfb_ctx* c, const float* h_in, float* logits_out, int head_m
 // ===========================================================================
 // Batched decode (BASELINE.json configs[3]): see csrc/nfb_batch.cu.
 // ===========================================================================
-static int bgemm(nfb_ctx* c, bool ta, int m, int n, int k, const uint16_t* A, int lda, const uint16_t* B, int ldb,
-                 float* C, int ldc) {
-  const float one = 1.f, zero = 0.f;
-  const cublasStatus_t st =
-      cublasGemmEx((cublasHandle_t)c->cublas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_OP_N, m, n, k, &one, A,
-                   CUDA_R_16F, lda, B, CUDA_R_16F, ldb, &zero, C, CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
-                   CUBLAS_GEMM_DEFAULT);
-  if (st != CUBLAS_STATUS_SUCCESS) return fail(NFB_ECUDA, "cublasGemmEx failed (" + std::to_string((int)st) + ")");
+// Y[n][m] = sum_k W[m][k] A[n][k] on the tcgen05 GEMM (csrc/nfb_umma.cu).
+static int ugemm(nfb_ctx* c, cudaStream_t st, const CUtensorMap* tw, const CUtensorMap* ta, int M, int N, int K,
+                 float* Y) {
+  const cudaError_t e = umma_gemm(st, tw, ta, M, N, K, Y, c->uws, c->uctr, c->err, c->sm_count);
+  if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("umma_gemm launch: ") + cudaGetErrorString(e));
   return NFB_OK;
 }
 
-// Y[n][m] = sum_k W[m][k] A[n][k]: our skinny tensor-core kernel for N <= 32
-// activation rows, cuBLAS otherwise.  Wt: the same weights stored transposed
-// ([K][M], the fused kernel's layout) for the cuBLAS call; W may be null.
-static int rgemm(nfb_ctx* c, cudaStream_t st, int M, int N, int K, const uint16_t* W, const uint16_t* Wt,
-                 const uint16_t* A, float* Y) {
-  if (W && skinny_gemm(st, reinterpret_cast<const __half*>(W), reinterpret_cast<const __half*>(A), Y, M, N, K) == 0)
-    return NFB_OK;
-  if (Wt) return bgemm(c, false, M, N, K, Wt, M, A, K, Y, M);
-  return bgemm(c, true, M, N, K, W, K, A, K, Y, M);
-}
-
-// (Re)build the row-major W_out / W_down copies after a weight change.
-static void batch_prepare(nfb_ctx* c, cudaStream_t st) {
-  if (c->bwo.empty() || c->bt_ver == c->wver) return;
-  const int h = c->desc.hidden, mm = c->desc.d_mlp;
-  for (int l = 0; l < c->desc.n_layers; ++l) {
-    transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].woT), reinterpret_cast<__half*>(c->bwo[l]), h, h);
-    transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].wdT), reinterpret_cast<__half*>(c->bwd[l]), mm, h);
+// (Re)build the row-major W_out / W_down copies and the weight tensor maps
+// after a weight change; the activation maps when the batch size changes.
+static int batch_prepare(nfb_ctx* c, cudaStream_t st) {
+  const int h = c->desc.hidden, mm = c->desc.d_mlp, L = c->desc.n_layers, V = c->desc.vocab;
+  if (c->bt_ver != c->wver) {
+    for (int l = 0; l < L; ++l) {
+      transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].woT), reinterpret_cast<__half*>(c->bwo[l]), h, h);
+      transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].wdT), reinterpret_cast<__half*>(c->bwd[l]), mm, h);
+    }
+    CK(cudaGetLastError());
+    c->bmap_w.resize((size_t)4 * L);
+    for (int l = 0; l < L; ++l) {
+      CUtensorMap* mp = &c->bmap_w[(size_t)4 * l];
+      if (make_tmap_f16(mp + 0, c->layers[l].wqkv, h, (uint64_t)3 * h, h, 128) ||
+          make_tmap_f16(mp + 1, c->bwo[l], h, h, h, 128) || make_tmap_f16(mp + 2, c->layers[l].wup, h, mm, h, 128) ||
+          make_tmap_f16(mp + 3, c->bwd[l], mm, h, mm, 128))
+        return fail(NFB_ECUDA, "cuTensorMapEncodeTiled failed (weights)");
+    }
+    if (make_tmap_f16(&c->bmap_lm, c->unembed, h, V, h, 128))
+      return fail(NFB_ECUDA, "cuTensorMapEncodeTiled failed (LM head)");
+    c->bt_ver = c->wver;
   }
-  c->bt_ver = c->wver;
+  if (c->bmap_rows != c->bcur) {
+    const int N = 2 * c->bcur, box = umma_n_pad(N);
+    const uint64_t rows = 2 * (uint64_t)c->bmax;
+    if (make_tmap_f16(&c->bmap_a1, c->ba1, h, rows, h, box) || make_tmap_f16(&c->bmap_a2, c->ba2, h, rows, h, box) ||
+        make_tmap_f16(&c->bmap_ctx, c->bctx, h, rows, h, box) || make_tmap_f16(&c->bmap_g, c->bg, mm, rows, mm, box))
+      return fail(NFB_ECUDA, "cuTensorMapEncodeTiled failed (activations)");
+    c->bmap_rows = c->bcur;
+  }
+  return NFB_OK;
 }
 
 // One token for all bcur sequences: layers (LN -> QKV GEMM -> RoPE/append ->
@@ -1462,18 +1484,19 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
   const nfb_model_desc& m = c->desc;
   const int B = c->bcur, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
   const int L = m.n_layers, S = c->bsplit;
-  cublasSetStream((cublasHandle_t)c->cublas, st);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cs);
-  if (cs == cudaStreamCaptureStatusNone) batch_prepare(c, st);
+  if (cs == cudaStreamCaptureStatusNone) TRY(batch_prepare(c, st));
+  else if (c->bt_ver != c->wver || c->bmap_rows != c->bcur)
+    return fail(NFB_ESTATE, "batched graph capture needs prepared tensor maps (call batch_prepare first)");
   if (in_token) embed_kernel<<<B, 256, 0, st>>>(c->btok, reinterpret_cast<const __half*>(c->embed), h, V, c->bx);
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   for (int l = 0; l < L; ++l) {
     const LayerBufs& w = c->layers[l];
+    const CUtensorMap* mw = &c->bmap_w[(size_t)4 * l];
     ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g, w.ln2b,
                                       reinterpret_cast<__half*>(c->ba1), reinterpret_cast<__half*>(c->ba2));
-    const bool sk = 2 * B <= 8 && !c->bwo.empty();
-    TRY(rgemm(c, st, 3 * h, 2 * B, h, w.wqkv, nullptr, c->ba1, c->by));
+    TRY(ugemm(c, st, mw + 0, &c->bmap_a1, 3 * h, 2 * B, h, c->by));
     // batch: sequence b has its own cache; prefill: the T prompt rows share
     // the context's cache at consecutive positions (causal)
     __half* kc = reinterpret_cast<__half*>(prefill ? w.kc : c->bkc[l]);
@@ -1485,17 +1508,17 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     attn_tile_kernel<<<dim3(B * H, S), 128, attn_tile_smem(d), st>>>(c->bq, kc, vc, B, H, d, c->max_seq, c->bstate,
                                                                      scale_log2, c->bpart, pstep, sstride);
     attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
-    TRY(rgemm(c, st, h, 2 * B, h, sk ? c->bwo[l] : nullptr, w.woT, c->bctx, c->bz));
-    TRY(rgemm(c, st, mm, 2 * B, h, w.wup, nullptr, c->ba2, c->bu));
+    TRY(ugemm(c, st, mw + 1, &c->bmap_ctx, h, 2 * B, h, c->bz));
+    TRY(ugemm(c, st, mw + 2, &c->bmap_a2, mm, 2 * B, h, c->bu));
     gelu_hilo_kernel<<<dim3(B, (mm + 255) / 256), 256, 0, st>>>(c->bu, B, mm, w.bup, m.gelu_exact,
                                                                 reinterpret_cast<__half*>(c->bg));
-    TRY(rgemm(c, st, h, 2 * B, mm, sk ? c->bwd[l] : nullptr, w.wdT, c->bg, c->bdn));
+    TRY(ugemm(c, st, mw + 3, &c->bmap_g, h, 2 * B, mm, c->bdn));
     residual_kernel<<<dim3(B, (h + 255) / 256), 256, 0, st>>>(c->bx, B, h, c->bz, w.bo, c->bdn, w.bd);
   }
   if (head) {
     ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, c->lnfg, c->lnfb, nullptr, nullptr,
                                       reinterpret_cast<__half*>(c->ba1), nullptr);
-    TRY(rgemm(c, st, V, 2 * B, h, c->unembed, nullptr, c->ba1, c->blg));
+    TRY(ugemm(c, st, &c->bmap_lm, &c->bmap_a1, V, 2 * B, h, c->blg));
     argmax_kernel<<<B, 1024, 0, st>>>(c->blg, B, V, c->btok, c->blogits);
   }
   advance_pos_kernel<<<1, 1, 0, st>>>(c->bstate);
@@ -1505,7 +1528,7 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
 
 int nfb_batch_init(nfb_ctx* c, int max_batch) {
   if (!c) return fail(NFB_EINVAL, "null context");
-  if (max_batch < 1 || max_batch > 1024) return fail(NFB_EINVAL, "max_batch must be in [1, 1024]");
+  if (max_batch < 1 || max_batch > 128) return fail(NFB_EINVAL, "max_batch must be in [1, 128] (UMMA N = 2B <= 256)");
   if (c->bmax) return fail(NFB_ESTATE, "batch buffers already allocated");
   if (c->tp_size > 1) return fail(NFB_EUNSUPPORTED, "batched decode is single-GPU");
   if (!c->desc.parallel_residual) return fail(NFB_EUNSUPPORTED, "batched decode needs the parallel residual");
@@ -1525,14 +1548,12 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   }
   c->bkc.resize(m.n_layers);
   c->bvc.resize(m.n_layers);
+  c->bwo.resize(m.n_layers);
+  c->bwd.resize(m.n_layers);
   int r = NFB_OK;
-  if (2 * B <= 8) {
-    c->bwo.resize(m.n_layers);
-    c->bwd.resize(m.n_layers);
-    for (int l = 0; l < m.n_layers; ++l)
-      if ((r = dalloc(c, &c->bwo[l], h * h)) || (r = dalloc(c, &c->bwd[l], h * mm))) return r;
-    c->bt_ver = 0;
-  }
+  for (int l = 0; l < m.n_layers; ++l)
+    if ((r = dalloc(c, &c->bwo[l], h * h)) || (r = dalloc(c, &c->bwd[l], h * mm))) return r;
+  c->bt_ver = 0;
   for (int l = 0; l < m.n_layers; ++l)
     if ((r = dalloc(c, &c->bkc[l], B * H * c->max_seq * d)) || (r = dalloc(c, &c->bvc[l], B * H * c->max_seq * d)))
       return r;
@@ -1543,13 +1564,25 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
       (r = dalloc(c, &c->bctx, 2 * B * h)) || (r = dalloc(c, &c->bg, 2 * B * mm)) || (r = dalloc(c, &c->btok, B)) ||
       (r = dalloc(c, &c->bstate, 4)))
     return r;
-  cublasHandle_t hb = nullptr;
-  if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) return fail(NFB_ECUDA, "cublasCreate failed");
-  c->cublas = hb;
-  const size_t ws = 32u << 20;
-  if (dalloc(c, reinterpret_cast<unsigned char**>(&c->cublas_ws), ws) != NFB_OK) return fail(NFB_ECUDA, "workspace");
-  cublasSetWorkspace(hb, c->cublas_ws, ws);  // fixed workspace: graph-capture safe
-  cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH);
+  // stream-K workspace: the largest tiles x pieces x n_pad x 128 over the
+  // five GEMM shapes (pieces depend on M, K and the grid only; n_pad is
+  // largest at the largest batch)
+  {
+    const int shapes[5][2] = {{3 * (int)h, (int)h}, {(int)h, (int)h}, {(int)mm, (int)h}, {(int)h, (int)mm}, {(int)V, (int)h}};
+    size_t need = 1;
+    int tiles_max = 1;
+    for (auto& sh : shapes) {
+      int grid = 0, mp = 0;
+      umma_plan(sh[0], 2 * (int)B, sh[1], c->sm_count, &grid, &mp);
+      const int tiles = (sh[0] + 127) / 128;
+      need = std::max(need, (size_t)tiles * mp * umma_n_pad(2 * (int)B) * 128);
+      tiles_max = std::max(tiles_max, tiles);
+    }
+    if ((r = dalloc(c, &c->uws, need)) || (r = dalloc(c, &c->uctr, tiles_max))) return r;
+    c->uws_floats = need;
+    c->uctr_n = tiles_max;
+  }
+  if (!umma_encoder_available()) return fail(NFB_EUNSUPPORTED, "cuTensorMapEncodeTiled unavailable (driver too old)");
   c->bmax = max_batch;
   return NFB_OK;
 }
@@ -1647,7 +1680,7 @@ int nfb_batch_step(nfb_ctx* c, int n, void* stream) {
   if (n < 0 || c->bpos + n > c->max_seq) return fail(NFB_EINVAL, "batch decode would exceed the KV capacity");
   cudaSetDevice(c->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-  if (c->bgexec) batch_prepare(c, st);  // the graph reads the copies in place
+  if (c->bgexec) TRY(batch_prepare(c, st));  // the graph reads the copies in place
   for (int i = 0; i < n; ++i) {
     if (c->bgexec) CK(cudaGraphLaunch(c->bgexec, st));
     else TRY(batch_token(c, st, true, true));
@@ -1669,7 +1702,7 @@ int nfb_batch_graph_capture(nfb_ctx* c) {
     cudaGraphDestroy(c->bgraph);
     c->bgraph = nullptr;
   }
-  batch_prepare(c, c->stream);
+  TRY(batch_prepare(c, c->stream));
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   const int r = batch_token(c, c->stream, true, true);
   cudaGraph_t g = nullptr;

@@ -1,12 +1,12 @@
 // Batched decode (BASELINE.json configs[3]: Pythia-2.8B batch sweep 1/4/16/64,
 // context 4096) -- B sequences at the same position, one token each per step.
 //
-// With B > 1 the projections become dense contractions: they run as cuBLAS
-// fp16 GEMMs (tensor cores, fp32 accumulation) over the weights in their
-// decode-kernel layout, fed with the activations split into fp16 hi + lo rows
+// With B > 1 the projections become dense contractions: they run on our
+// tcgen05 / TMEM / TMA GEMM (csrc/nfb_umma.cu) over the weights in their
+// row-major layout, fed with the activations split into fp16 hi + lo rows
 // (x = hi + lo to ~2^-22, so the products keep fp32-class precision at the
 // cost of a 2B-wide GEMM, still weight-bandwidth bound).  Everything between
-// the GEMMs is ours (nf/golden.py:189-228 semantics):
+// the GEMMs is here too (nf/golden.py:189-228 semantics):
 //   ln_hilo_kernel        LN1 / LN2 (two-pass, nf/golden.py:34-40) -> hi/lo rows
 //   attn_prep_kernel      QKV bias, partial RoPE (nf/golden.py:68-92), K/V append
 //   attn_tile_kernel      decode attention over 128-position KV tiles (bulk-copied
@@ -343,104 +343,6 @@ __global__ void advance_pos_kernel(int* state) { state[0] += 1; }
 }  // namespace nfb
 
 namespace nfb {
-
-// ---------------------------------------------------------------------------
-// Skinny GEMM for the batched path at N = 2B <= 32 activation rows:
-//   Y[n][m] = sum_k W[m][k] * A[n][k]    (W fp16 row-major [M][K], A fp16
-//   [N][K] hi / lo rows, Y fp32 [N][M]).
-// Weight-streaming bound: each warp owns 16 rows x K/8 and feeds mma.sync
-// m16n8k16 straight from 16-byte global loads.  The k order inside a 32-wide
-// step is permuted identically for W and A (lane (g, t) loads k0 + 8t .. +7 of
-// W rows g, g + 8 and of activation row g), so no shuffles or ldmatrix are
-// needed.  The 8 warps' partials are summed in fixed warp order (bitwise
-// reproducible).  Requires M % 16 == 0 and K % 256 == 0.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-template <int NT>
-__global__ void __launch_bounds__(256) skinny_gemm_kernel(const __half* __restrict__ W, const __half* __restrict__ A,
-                                                          float* __restrict__ Y, int M, int N, int K) {
-  __shared__ float red[8][NT * 4][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int m0 = blockIdx.x * 16, Kw = K >> 3, k0 = warp * Kw;
-  const __half* r0 = W + (size_t)(m0 + g) * K + k0 + 8 * t;
-  const __half* r1 = r0 + (size_t)8 * K;
-  const __half* ap[NT];
-  bool av[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int n = nt * 8 + g;
-    av[nt] = n < N;
-    ap[nt] = A + (size_t)(av[nt] ? n : 0) * K + k0 + 8 * t;
-  }
-  float acc[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
-  // U steps of 32 k: all weight and activation loads are issued before the
-  // first mma (the empty asm with a memory clobber keeps ptxas from sinking
-  // the loads next to their uses, which would leave ~2 loads in flight)
-  constexpr int U = NT == 1 ? 8 : 4;
-  auto block = [&](int k, int nu) {
-    uint4 wa[U], wb[U], x[U][NT];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (u < nu) {
-        wa[u] = __ldcs(reinterpret_cast<const uint4*>(r0 + k + 32 * u));
-        wb[u] = __ldcs(reinterpret_cast<const uint4*>(r1 + k + 32 * u));
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          x[u][nt] = av[nt] ? __ldg(reinterpret_cast<const uint4*>(ap[nt] + k + 32 * u)) : make_uint4(0u, 0u, 0u, 0u);
-      }
-    asm volatile("" ::: "memory");
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (u < nu)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          mma16816(acc[nt], wa[u].x, wb[u].x, wa[u].y, wb[u].y, x[u][nt].x, x[u][nt].y);
-          mma16816(acc[nt], wa[u].z, wb[u].z, wa[u].w, wb[u].w, x[u][nt].z, x[u][nt].w);
-        }
-  };
-  int k = 0;
-  for (; k + 32 * U <= Kw; k += 32 * U) block(k, U);
-  if (k < Kw) block(k, (Kw - k) >> 5);
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) red[warp][nt * 4 + i][lane] = acc[nt][i];
-  __syncthreads();
-  for (int e = threadIdx.x; e < NT * 4 * 32; e += blockDim.x) {
-    const int ai = e >> 5, ln = e & 31;
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s += red[w][ai][ln];
-    const int nt = ai >> 2, i = ai & 3;
-    const int m = m0 + (ln >> 2) + (i >= 2 ? 8 : 0), n = nt * 8 + 2 * (ln & 3) + (i & 1);
-    if (n < N) Y[(size_t)n * M + m] = s;
-  }
-}
-
-int skinny_gemm(cudaStream_t st, const __half* W, const __half* A, float* Y, int M, int N, int K) {
-  // N > 8: cuBLAS is faster (B = 16: 2842 vs 2282 tok/s with this kernel)
-  if (N < 1 || N > 8 || M % 16 || K % 256) return -1;
-  const dim3 grid(M / 16);
-  switch ((N + 7) / 8) {
-    case 1: skinny_gemm_kernel<1><<<grid, 256, 0, st>>>(W, A, Y, M, N, K); break;
-    case 2: skinny_gemm_kernel<2><<<grid, 256, 0, st>>>(W, A, Y, M, N, K); break;
-    case 3: skinny_gemm_kernel<3><<<grid, 256, 0, st>>>(W, A, Y, M, N, K); break;
-    default: skinny_gemm_kernel<4><<<grid, 256, 0, st>>>(W, A, Y, M, N, K); break;
-  }
-  return 0;
-}
 
 // out[c][r] = in[r][c] (fp16, rows x cols), 32 x 32 tiles
 __global__ void transpose_f16_kernel(const __half* in, __half* out, int rows, int cols) {

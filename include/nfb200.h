@@ -209,6 +209,14 @@ int nfb_batch_read_tokens(nfb_ctx* ctx, int* tokens);
  * hold exactly `pos` positions), final hidden states to x_out (optional).
  * Runs on the batched kernels in chunks of max_batch rows (nfb_batch_init). */
 int nfb_prefill(nfb_ctx* ctx, int pos, int count, const float* x_in, float* x_out);
+/* Diagnostics: the batched-projection GEMM (csrc/nfb_umma.cu, tcgen05 + TMA,
+ * stream-K with a deterministic fixup) on caller-owned DEVICE buffers:
+ * Y[N][M] (fp32) = W[M][K] (fp16, row-major) . A[N][K]^T (fp16), N <= 256,
+ * K % 8 == 0, enqueued on `stream` (NULL = legacy default).  Not in the
+ * reference; used by the unit test / microbenchmark of that kernel.  Returns 0
+ * or a negative code.  Not thread-safe (one shared workspace). */
+int nfb_gemm_f16_dev(int M, int N, int K, const void* W, const void* A, float* Y, void* stream);
+
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
 

@@ -68,6 +68,7 @@ SIGNATURES = {
     "nfb_block_step": (_I, [_P, _I, _I, _FP, _FP]),
     "nfb_forward": (_I, [_P, _I, _FP, _FP, _FP, _I]),
     "nfb_block_step_dev": (_I, [_P, _I, _I, _P, _P, _P]),
+    "nfb_gemm_f16_dev": (_I, [_I, _I, _I, _P, _P, _P, _P]),
     "nfb_forward_dev": (_I, [_P, _I, _P, _P, _P, _I, _P]),
     "nfb_begin_decode": (_I, [_P, _I, _I]),
     "nfb_decode_step": (_I, [_P, _P]),
