@@ -17,34 +17,35 @@
 
 #include "../include/nfb200.h"
 #include "nfb_internal.h"
+#include "nfb_umma.cuh"
 
 namespace nfb {
 const void* decode_kernel_ptr(int dpl);
 // batched decode kernels (csrc/nfb_batch.cu)
 __global__ void ln_hilo_kernel(const float* x, int B, int h, float eps, const float* g1, const float* b1,
-                               const float* g2, const float* b2, __half* a1, __half* a2);
-__global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, const int* state, int max_seq,
+                               const float* g2, const float* b2, __half* a1, __half* a2, int n_pad);
+__global__ void attn_prep_kernel(const UOut y, int B, int H, int d, int rd, const int* state, int max_seq,
                                  const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc,
                                  int pos_step, size_t seq_stride);
-__global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx);
+__global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx, int n_pad);
 __global__ void attn_tile_kernel(const float* q, const __half* kc, const __half* vc, int B, int H, int d,
                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
                                  size_t seq_stride);
 size_t attn_tile_smem(int d);
 // tcgen05 GEMM (csrc/nfb_umma.cu)
-int make_tmap_f16(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows, uint64_t ld, int box_rows);
-bool umma_encoder_available();
-int umma_n_pad(int N);
-void umma_plan(int M, int N, int K, int sm_count, int* grid, int* max_pieces);
-cudaError_t umma_gemm(cudaStream_t st, const CUtensorMap* tw, const CUtensorMap* ta, int M, int N, int K, float* Y,
-                      float* ws, int* counters, int* err, int sm_count);
-void transpose_f16(cudaStream_t st, const __half* in, __half* out, int rows, int cols);
-__global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g);
-__global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
+UPlan umma_plan(int M, int N, int K, int sm_count);
+size_t umma_blocked_elems(int M, int K);
+size_t umma_act_elems(int n_pad, int K);
+UOut umma_out(const UPlan& P, const float* ws);
+void umma_block_weights(cudaStream_t st, const __half* src, int M, int K, size_t ld, bool trans, __half* dst);
+cudaError_t umma_gemm(cudaStream_t st, const UPlan& P, const void* Wb, const void* Ab, float* ws, int* err, bool pdl,
+                      unsigned long long* trace = nullptr);
+__global__ void gelu_hilo_kernel(const UOut u, int B, int m, const float* bup, int exact, __half* g, int n_pad);
+__global__ void residual_kernel(float* x, int B, int h, const UOut z, const float* bo, const UOut dn,
                                 const float* bd);
-__global__ void argmax_kernel(const float* lg, int B, int V, int* tokens, float* logits_out);
+__global__ void argmax_kernel(const UOut lg, int B, int V, unsigned long long* amax, float* logits_out);
 __global__ void embed_kernel(const int* tokens, const __half* embed, int h, int V, float* x);
-__global__ void advance_pos_kernel(int* state);
+__global__ void advance_kernel(int* state, unsigned long long* amax, int* tokens, int B, int V);
 cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
                           bool cooperative);
 cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out);
@@ -291,27 +292,30 @@ struct nfb_ctx {
   void* nccl = nullptr;   // ncclComm_t
   // batched decode (nfb_batch_*): B sequences at one position, tcgen05 GEMMs
   int bmax = 0, bcur = 0, bsplit = 1;
-  // row-major W_out / W_down ([h][h], [h][d_mlp]: K-major UMMA operands),
-  // rebuilt from the decode kernel's transposed copies when the weights
-  // change (wver)
-  std::vector<uint16_t*> bwo, bwd;
+  // blocked (UMMA SW128) copies of every projection, per layer [qkv, out,
+  // up, down] + the LM head (csrc/nfb_umma.cuh), rebuilt from the decode
+  // kernel's copies when the weights change (wver)
+  std::vector<uint16_t*> bw;  // [layer * 4 + j]
+  uint16_t* blm = nullptr;
   unsigned long long wver = 1, bt_ver = 0;
   std::vector<uint16_t*> bkc, bvc;  // per layer [bmax][H][max_seq][d]
-  float *bx = nullptr, *by = nullptr, *bq = nullptr, *bpart = nullptr, *bz = nullptr, *bu = nullptr,
-        *bdn = nullptr, *blg = nullptr, *blogits = nullptr;
+  float *bx = nullptr, *bq = nullptr, *bpart = nullptr, *blogits = nullptr;
+  // blocked activation operands (hi / lo rows, n_pad of the largest batch)
   uint16_t *ba1 = nullptr, *ba2 = nullptr, *bctx = nullptr, *bg = nullptr;
   int *btok = nullptr, *bstate = nullptr;
+  unsigned long long* bamax = nullptr;  // [bmax] packed argmax of the step
   int bpos = -1;
-  // TMA tensor maps: per layer [qkv, out, up, down] weights, the LM head, and
-  // the activation operands for the current batch (rebuilt when it changes)
-  std::vector<CUtensorMap> bmap_w;  // [layer * 4 + j]
-  CUtensorMap bmap_lm{};
-  CUtensorMap bmap_a1{}, bmap_a2{}, bmap_ctx{}, bmap_g{};
-  int bmap_rows = 0;                 // batch the activation maps were built for
-  float* uws = nullptr;              // stream-K partials
-  int* uctr = nullptr;               // stream-K tile counters
-  size_t uws_floats = 0;
-  int uctr_n = 0;
+  // the MLP branch (LN2 -> up -> GELU -> down) runs on a second stream,
+  // concurrently with the attention branch (the parallel residual makes them
+  // independent); forked / joined with events (graph-capturable)
+  cudaStream_t bstream2 = nullptr;
+  cudaEvent_t bev[2] = {nullptr, nullptr};
+  int bfork = 1;
+  // stream-K partials per GEMM role [qkv, out, up, down, lm] (the consumer
+  // kernels sum the pieces) and the plans of the current batch
+  float* uws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  UPlan uplan[5] = {};
+  int uplan_rows = 0;
   cudaGraph_t bgraph = nullptr;
   cudaGraphExec_t bgexec = nullptr;
   unsigned long long* gbar = nullptr;
@@ -347,6 +351,25 @@ int dalloc(nfb_ctx* c, T** p, size_t n) {
   c->allocs.push_back(q);
   *p = static_cast<T*>(q);
   return NFB_OK;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor runs; it griddepcontrol.wait's before
+// touching the predecessor's results (csrc/nfb_batch.cu, csrc/nfb_umma.cu).
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 #define TRY(expr)              \
@@ -746,6 +769,9 @@ int nfb_destroy(nfb_ctx* c) {
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->h_tok) cudaFreeHost(c->h_tok);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->bstream2) cudaStreamDestroy(c->bstream2);
+  for (auto& e : c->bev)
+    if (e) cudaEventDestroy(e);
   delete c;
   return NFB_OK;
 }
@@ -904,6 +930,7 @@ int nfb_set_head(nfb_ctx* c, const void* embed, const void* lnf_gain, const void
   if (unembed) {
     TRY(upload_f16(unembed, dtype, V, h, L_ROW, c->unembed));
     c->has_unembed = true;
+    ++c->wver;  // the batched path's blocked LM-head copy
   }
   return NFB_OK;
 }
@@ -922,6 +949,7 @@ int nfb_synth_head(nfb_ctx* c, uint64_t seed) {
                          std::sqrt((double)h), c->unembed, nullptr));
   CK(cudaStreamSynchronize(st));
   c->has_embed = c->has_lnf = c->has_unembed = true;
+  ++c->wver;
   return NFB_OK;
 }
 
@@ -1436,43 +1464,37 @@ int nfb_head_logits(nfb_ctx* c, const float* h_in, float* logits_out, int head_m
 // ===========================================================================
 // Batched decode (BASELINE.json configs[3]): see csrc/nfb_batch.cu.
 // ===========================================================================
-// Y[n][m] = sum_k W[m][k] A[n][k] on the tcgen05 GEMM (csrc/nfb_umma.cu).
-static int ugemm(nfb_ctx* c, cudaStream_t st, const CUtensorMap* tw, const CUtensorMap* ta, int M, int N, int K,
-                 float* Y) {
-  const cudaError_t e = umma_gemm(st, tw, ta, M, N, K, Y, c->uws, c->uctr, c->err, c->sm_count);
+// Y = W . A on the tcgen05 GEMM (csrc/nfb_umma.cu): role j of the current
+// plan set (0 qkv, 1 out, 2 up, 3 down, 4 lm).
+static int ugemm(nfb_ctx* c, cudaStream_t st, int j, const void* Wb, const void* Ab) {
+  const cudaError_t e = umma_gemm(st, c->uplan[j], Wb, Ab, c->uws[j], c->err, true);
   if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("umma_gemm launch: ") + cudaGetErrorString(e));
   return NFB_OK;
 }
 
-// (Re)build the row-major W_out / W_down copies and the weight tensor maps
-// after a weight change; the activation maps when the batch size changes.
+// (Re)build the blocked weight copies after a weight change, and the GEMM
+// plans when the batch size changes.
 static int batch_prepare(nfb_ctx* c, cudaStream_t st) {
   const int h = c->desc.hidden, mm = c->desc.d_mlp, L = c->desc.n_layers, V = c->desc.vocab;
   if (c->bt_ver != c->wver) {
     for (int l = 0; l < L; ++l) {
-      transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].woT), reinterpret_cast<__half*>(c->bwo[l]), h, h);
-      transpose_f16(st, reinterpret_cast<const __half*>(c->layers[l].wdT), reinterpret_cast<__half*>(c->bwd[l]), mm, h);
+      const LayerBufs& w = c->layers[l];
+      __half** bw = reinterpret_cast<__half**>(&c->bw[(size_t)4 * l]);
+      umma_block_weights(st, reinterpret_cast<const __half*>(w.wqkv), 3 * h, h, h, false, bw[0]);
+      umma_block_weights(st, reinterpret_cast<const __half*>(w.woT), h, h, h, true, bw[1]);    // W_out = woT^T
+      umma_block_weights(st, reinterpret_cast<const __half*>(w.wup), mm, h, h, false, bw[2]);
+      umma_block_weights(st, reinterpret_cast<const __half*>(w.wdT), h, mm, h, true, bw[3]);   // W_down = wdT^T
     }
+    if (c->has_unembed)
+      umma_block_weights(st, reinterpret_cast<const __half*>(c->unembed), V, h, h, false,
+                         reinterpret_cast<__half*>(c->blm));
     CK(cudaGetLastError());
-    c->bmap_w.resize((size_t)4 * L);
-    for (int l = 0; l < L; ++l) {
-      CUtensorMap* mp = &c->bmap_w[(size_t)4 * l];
-      if (make_tmap_f16(mp + 0, c->layers[l].wqkv, h, (uint64_t)3 * h, h, 128) ||
-          make_tmap_f16(mp + 1, c->bwo[l], h, h, h, 128) || make_tmap_f16(mp + 2, c->layers[l].wup, h, mm, h, 128) ||
-          make_tmap_f16(mp + 3, c->bwd[l], mm, h, mm, 128))
-        return fail(NFB_ECUDA, "cuTensorMapEncodeTiled failed (weights)");
-    }
-    if (make_tmap_f16(&c->bmap_lm, c->unembed, h, V, h, 128))
-      return fail(NFB_ECUDA, "cuTensorMapEncodeTiled failed (LM head)");
     c->bt_ver = c->wver;
   }
-  if (c->bmap_rows != c->bcur) {
-    const int N = 2 * c->bcur, box = umma_n_pad(N);
-    const uint64_t rows = 2 * (uint64_t)c->bmax;
-    if (make_tmap_f16(&c->bmap_a1, c->ba1, h, rows, h, box) || make_tmap_f16(&c->bmap_a2, c->ba2, h, rows, h, box) ||
-        make_tmap_f16(&c->bmap_ctx, c->bctx, h, rows, h, box) || make_tmap_f16(&c->bmap_g, c->bg, mm, rows, mm, box))
-      return fail(NFB_ECUDA, "cuTensorMapEncodeTiled failed (activations)");
-    c->bmap_rows = c->bcur;
+  if (c->uplan_rows != c->bcur) {
+    const int shapes[5][2] = {{3 * h, h}, {h, h}, {mm, h}, {h, mm}, {V, h}};
+    for (int j = 0; j < 5; ++j) c->uplan[j] = umma_plan(shapes[j][0], 2 * c->bcur, shapes[j][1], c->sm_count);
+    c->uplan_rows = c->bcur;
   }
   return NFB_OK;
 }
@@ -1480,6 +1502,7 @@ static int batch_prepare(nfb_ctx* c, cudaStream_t st) {
 // One token for all bcur sequences: layers (LN -> QKV GEMM -> RoPE/append ->
 // split-KV attention -> W_out GEMM, LN2 -> up GEMM -> GELU -> down GEMM ->
 // residual) then final LN -> LM GEMM -> argmax.  in_token: x from btok.
+// Every launch carries the PDL attribute (launch_pdl / umma_gemm).
 static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bool prefill = false) {
   const nfb_model_desc& m = c->desc;
   const int B = c->bcur, h = m.hidden, H = m.n_heads, d = m.d_head, mm = m.d_mlp, V = m.vocab;
@@ -1487,42 +1510,61 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cs);
   if (cs == cudaStreamCaptureStatusNone) TRY(batch_prepare(c, st));
-  else if (c->bt_ver != c->wver || c->bmap_rows != c->bcur)
-    return fail(NFB_ESTATE, "batched graph capture needs prepared tensor maps (call batch_prepare first)");
-  if (in_token) embed_kernel<<<B, 256, 0, st>>>(c->btok, reinterpret_cast<const __half*>(c->embed), h, V, c->bx);
+  else if (c->bt_ver != c->wver || c->uplan_rows != c->bcur)
+    return fail(NFB_ESTATE, "batched graph capture needs prepared weights / plans (call batch_prepare first)");
+  const int np = c->uplan[0].n_pad;
+  __half* a1 = reinterpret_cast<__half*>(c->ba1);
+  __half* a2 = reinterpret_cast<__half*>(c->ba2);
+  __half* actx = reinterpret_cast<__half*>(c->bctx);
+  __half* ag = reinterpret_cast<__half*>(c->bg);
+  const UOut oq = umma_out(c->uplan[0], c->uws[0]), oz = umma_out(c->uplan[1], c->uws[1]);
+  const UOut ou = umma_out(c->uplan[2], c->uws[2]), od = umma_out(c->uplan[3], c->uws[3]);
+  if (in_token)
+    CK(launch_pdl(embed_kernel, dim3(B), dim3(256), 0, st, c->btok, reinterpret_cast<const __half*>(c->embed), h, V,
+                  c->bx));
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   for (int l = 0; l < L; ++l) {
     const LayerBufs& w = c->layers[l];
-    const CUtensorMap* mw = &c->bmap_w[(size_t)4 * l];
-    ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g, w.ln2b,
-                                      reinterpret_cast<__half*>(c->ba1), reinterpret_cast<__half*>(c->ba2));
-    TRY(ugemm(c, st, mw + 0, &c->bmap_a1, 3 * h, 2 * B, h, c->by));
+    uint16_t* const* bw = &c->bw[(size_t)4 * l];
+    CK(launch_pdl(ln_hilo_kernel, dim3(B), dim3(256), 0, st, c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g,
+                  w.ln2b, a1, a2, np));
+    TRY(ugemm(c, st, 0, bw[0], a1));
     // batch: sequence b has its own cache; prefill: the T prompt rows share
     // the context's cache at consecutive positions (causal)
     __half* kc = reinterpret_cast<__half*>(prefill ? w.kc : c->bkc[l]);
     __half* vc = reinterpret_cast<__half*>(prefill ? w.vc : c->bvc[l]);
     const size_t sstride = prefill ? 0 : (size_t)H * c->max_seq * d;
     const int pstep = prefill ? 1 : 0;
-    attn_prep_kernel<<<dim3(B, H), 128, 3 * d * 4, st>>>(c->by, B, H, d, m.rotary_dims, c->bstate, c->max_seq,
-                                                         w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride);
-    attn_tile_kernel<<<dim3(B * H, S), 128, attn_tile_smem(d), st>>>(c->bq, kc, vc, B, H, d, c->max_seq, c->bstate,
-                                                                     scale_log2, c->bpart, pstep, sstride);
-    attn_combine_kernel<<<B * H, 128, 0, st>>>(c->bpart, S, B, H, d, reinterpret_cast<__half*>(c->bctx));
-    TRY(ugemm(c, st, mw + 1, &c->bmap_ctx, h, 2 * B, h, c->bz));
-    TRY(ugemm(c, st, mw + 2, &c->bmap_a2, mm, 2 * B, h, c->bu));
-    gelu_hilo_kernel<<<dim3(B, (mm + 255) / 256), 256, 0, st>>>(c->bu, B, mm, w.bup, m.gelu_exact,
-                                                                reinterpret_cast<__half*>(c->bg));
-    TRY(ugemm(c, st, mw + 3, &c->bmap_g, h, 2 * B, mm, c->bdn));
-    residual_kernel<<<dim3(B, (h + 255) / 256), 256, 0, st>>>(c->bx, B, h, c->bz, w.bo, c->bdn, w.bd);
+    // MLP branch (independent of the attention under the parallel residual)
+    cudaStream_t sm = st;
+    if (c->bfork) {
+      CK(cudaEventRecord(c->bev[0], st));
+      CK(cudaStreamWaitEvent(c->bstream2, c->bev[0], 0));
+      sm = c->bstream2;
+    }
+    TRY(ugemm(c, sm, 2, bw[2], a2));
+    CK(launch_pdl(gelu_hilo_kernel, dim3(B, (mm + 255) / 256), dim3(256), 0, sm, ou, B, mm, w.bup, m.gelu_exact,
+                  ag, np));
+    TRY(ugemm(c, sm, 3, bw[3], ag));
+    if (c->bfork) CK(cudaEventRecord(c->bev[1], sm));
+    CK(launch_pdl(attn_prep_kernel, dim3(B, H), dim3(128), (size_t)3 * d * 4, st, oq, B, H, d, m.rotary_dims,
+                  c->bstate, c->max_seq, w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride));
+    CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(128), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
+                  c->max_seq, c->bstate, scale_log2, c->bpart, pstep, sstride));
+    CK(launch_pdl(attn_combine_kernel, dim3(B * H), dim3(128), 0, st, c->bpart, S, B, H, d, actx, np));
+    TRY(ugemm(c, st, 1, bw[1], actx));
+    if (c->bfork) CK(cudaStreamWaitEvent(st, c->bev[1], 0));
+    CK(launch_pdl(residual_kernel, dim3(B, (h + 255) / 256), dim3(256), 0, st, c->bx, B, h, oz, w.bo, od, w.bd));
   }
   if (head) {
-    ln_hilo_kernel<<<B, 256, 0, st>>>(c->bx, B, h, (float)m.ln_eps, c->lnfg, c->lnfb, nullptr, nullptr,
-                                      reinterpret_cast<__half*>(c->ba1), nullptr);
-    TRY(ugemm(c, st, &c->bmap_lm, &c->bmap_a1, V, 2 * B, h, c->blg));
-    argmax_kernel<<<B, 1024, 0, st>>>(c->blg, B, V, c->btok, c->blogits);
+    CK(launch_pdl(ln_hilo_kernel, dim3(B), dim3(256), 0, st, c->bx, B, h, (float)m.ln_eps, c->lnfg, c->lnfb,
+                  (const float*)nullptr, (const float*)nullptr, a1, (__half*)nullptr, np));
+    TRY(ugemm(c, st, 4, c->blm, a1));
+    CK(launch_pdl(argmax_kernel, dim3(B, 37), dim3(256), 0, st, umma_out(c->uplan[4], c->uws[4]), B, V, c->bamax,
+                  c->blogits));
   }
-  advance_pos_kernel<<<1, 1, 0, st>>>(c->bstate);
-  CK(cudaGetLastError());
+  CK(launch_pdl(advance_kernel, dim3(1), dim3(128), 0, st, c->bstate, head ? c->bamax : (unsigned long long*)nullptr,
+                c->btok, B, V));
   return NFB_OK;
 }
 
@@ -1548,41 +1590,33 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   }
   c->bkc.resize(m.n_layers);
   c->bvc.resize(m.n_layers);
-  c->bwo.resize(m.n_layers);
-  c->bwd.resize(m.n_layers);
+  c->bw.resize((size_t)4 * m.n_layers);
   int r = NFB_OK;
+  const int shapes[5][2] = {{3 * (int)h, (int)h}, {(int)h, (int)h}, {(int)mm, (int)h}, {(int)h, (int)mm}, {(int)V, (int)h}};
   for (int l = 0; l < m.n_layers; ++l)
-    if ((r = dalloc(c, &c->bwo[l], h * h)) || (r = dalloc(c, &c->bwd[l], h * mm))) return r;
+    for (int j = 0; j < 4; ++j)
+      if ((r = dalloc(c, &c->bw[(size_t)4 * l + j], umma_blocked_elems(shapes[j][0], shapes[j][1])))) return r;
+  if ((r = dalloc(c, &c->blm, umma_blocked_elems((int)V, (int)h)))) return r;
   c->bt_ver = 0;
   for (int l = 0; l < m.n_layers; ++l)
     if ((r = dalloc(c, &c->bkc[l], B * H * c->max_seq * d)) || (r = dalloc(c, &c->bvc[l], B * H * c->max_seq * d)))
       return r;
-  if ((r = dalloc(c, &c->bx, B * h)) || (r = dalloc(c, &c->by, 2 * B * 3 * h)) || (r = dalloc(c, &c->bq, B * h)) ||
-      (r = dalloc(c, &c->bpart, B * H * c->bsplit * (d + 2))) || (r = dalloc(c, &c->bz, 2 * B * h)) ||
-      (r = dalloc(c, &c->bu, 2 * B * mm)) || (r = dalloc(c, &c->bdn, 2 * B * h)) || (r = dalloc(c, &c->blg, 2 * B * V)) ||
-      (r = dalloc(c, &c->blogits, B * V)) || (r = dalloc(c, &c->ba1, 2 * B * h)) || (r = dalloc(c, &c->ba2, 2 * B * h)) ||
-      (r = dalloc(c, &c->bctx, 2 * B * h)) || (r = dalloc(c, &c->bg, 2 * B * mm)) || (r = dalloc(c, &c->btok, B)) ||
-      (r = dalloc(c, &c->bstate, 4)))
+  const int npm = (2 * (int)B + 7) / 8 * 8;  // n_pad of the largest batch
+  if ((r = dalloc(c, &c->bx, B * h)) || (r = dalloc(c, &c->bq, B * h)) ||
+      (r = dalloc(c, &c->bpart, B * H * c->bsplit * (d + 2))) || (r = dalloc(c, &c->blogits, B * V)) ||
+      (r = dalloc(c, &c->ba1, umma_act_elems(npm, (int)h))) || (r = dalloc(c, &c->ba2, umma_act_elems(npm, (int)h))) ||
+      (r = dalloc(c, &c->bctx, umma_act_elems(npm, (int)h))) || (r = dalloc(c, &c->bg, umma_act_elems(npm, (int)mm))) ||
+      (r = dalloc(c, &c->btok, B)) || (r = dalloc(c, &c->bstate, 4)) || (r = dalloc(c, &c->bamax, B)))
     return r;
-  // stream-K workspace: the largest tiles x pieces x n_pad x 128 over the
-  // five GEMM shapes (pieces depend on M, K and the grid only; n_pad is
-  // largest at the largest batch)
-  {
-    const int shapes[5][2] = {{3 * (int)h, (int)h}, {(int)h, (int)h}, {(int)mm, (int)h}, {(int)h, (int)mm}, {(int)V, (int)h}};
-    size_t need = 1;
-    int tiles_max = 1;
-    for (auto& sh : shapes) {
-      int grid = 0, mp = 0;
-      umma_plan(sh[0], 2 * (int)B, sh[1], c->sm_count, &grid, &mp);
-      const int tiles = (sh[0] + 127) / 128;
-      need = std::max(need, (size_t)tiles * mp * umma_n_pad(2 * (int)B) * 128);
-      tiles_max = std::max(tiles_max, tiles);
-    }
-    if ((r = dalloc(c, &c->uws, need)) || (r = dalloc(c, &c->uctr, tiles_max))) return r;
-    c->uws_floats = need;
-    c->uctr_n = tiles_max;
-  }
-  if (!umma_encoder_available()) return fail(NFB_EUNSUPPORTED, "cuTensorMapEncodeTiled unavailable (driver too old)");
+  CK(cudaStreamCreateWithFlags(&c->bstream2, cudaStreamNonBlocking));
+  for (auto& e : c->bev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (getenv("NFB_BATCH_FORK")) c->bfork = atoi(getenv("NFB_BATCH_FORK"));
+  // stream-K partials per role: tiles x pieces x n_pad x 128 (pieces depend
+  // on M, K and the grid only; n_pad is largest at the largest batch)
+  for (int j = 0; j < 5; ++j)
+    if ((r = dalloc(c, &c->uws[j], umma_plan(shapes[j][0], 2 * (int)B, shapes[j][1], c->sm_count).ws_floats())))
+      return r;
+  c->uplan_rows = 0;
   c->bmax = max_batch;
   return NFB_OK;
 }

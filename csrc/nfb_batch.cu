@@ -2,11 +2,17 @@
 // context 4096) -- B sequences at the same position, one token each per step.
 //
 // With B > 1 the projections become dense contractions: they run on our
-// tcgen05 / TMEM / TMA GEMM (csrc/nfb_umma.cu) over the weights in their
-// row-major layout, fed with the activations split into fp16 hi + lo rows
-// (x = hi + lo to ~2^-22, so the products keep fp32-class precision at the
-// cost of a 2B-wide GEMM, still weight-bandwidth bound).  Everything between
-// the GEMMs is here too (nf/golden.py:189-228 semantics):
+// tcgen05 / TMEM GEMM (csrc/nfb_umma.cu) over blocked copies of the weights,
+// fed with the activations split into fp16 hi + lo rows (x = hi + lo to
+// ~2^-22, so the products keep fp32-class precision at the cost of a 2B-wide
+// GEMM, still weight-bandwidth bound).  The kernels here write those rows
+// directly in the GEMM's blocked SW128 layout (`ablk`) and read GEMM results
+// through `uout`, which sums the stream-K pieces in fixed order (the split-K
+// fixup, csrc/nfb_umma.cuh).  Every kernel opens with griddepcontrol.wait and
+// (except the many-wave attention tiles) releases its successor at once, so
+// under programmatic dependent launch the next GEMM's weight stream starts
+// while the small kernels run.  Everything between the GEMMs
+// (nf/golden.py:189-228 semantics):
 //   ln_hilo_kernel        LN1 / LN2 (two-pass, nf/golden.py:34-40) -> hi/lo rows
 //   attn_prep_kernel      QKV bias, partial RoPE (nf/golden.py:68-92), K/V append
 //   attn_tile_kernel      decode attention over 128-position KV tiles (bulk-copied
@@ -14,13 +20,15 @@
 //   attn_combine_kernel   log-sum-exp merge of the splits (nf/golden.py:128-136)
 //   gelu_hilo_kernel      up bias + GELU (nf/golden.py:156-166) -> hi/lo rows
 //   residual_kernel       x += W_o ctx + b_o + W_down g + b_down (parallel residual)
-//   argmax_kernel         greedy token per sequence (nf/fidelity.py:27-34)
+//   argmax_kernel         greedy token per sequence (nf/fidelity.py:27-34), vocab
+//                         chunks + packed atomicMax; advance_kernel -> tokens
 //   embed_kernel          token -> embedding row
 #include <cuda_fp16.h>
 #include <cstdint>
 
 #include "nfb_internal.h"
 #include "nfb_ptx.cuh"
+#include "nfb_umma.cuh"
 
 namespace nfb {
 
@@ -48,10 +56,11 @@ __device__ __forceinline__ float block_max(float v, float* sh) {
   return t;
 }
 
-__device__ __forceinline__ void put_hilo(__half* hi, __half* lo, int i, float v) {
-  const __half a = __float2half_rn(v);
-  hi[i] = a;
-  lo[i] = __float2half_rn(v - __half2float(a));
+// v -> blocked activation rows b (hi) and B + b (lo), column k
+__device__ __forceinline__ void put_hilo(__half* a, int b, int B, int n_pad, int k, float v) {
+  const __half hv = __float2half_rn(v);
+  a[ablk(b, k, n_pad)] = hv;
+  a[ablk(B + b, k, n_pad)] = __float2half_rn(v - __half2float(hv));
 }
 
 // grid B, block 256; x [B][h] fp32 (h <= 4096) -> A1 / A2 [2B][h] fp16 (rows
@@ -60,18 +69,23 @@ __device__ __forceinline__ void put_hilo(__half* hi, __half* lo, int i, float v)
 __device__ __forceinline__ float4 ld4(const float* p, int i4, bool ok) {
   return ok ? __ldg(reinterpret_cast<const float4*>(p) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
 }
-__device__ __forceinline__ void put_hilo4(__half* hi, __half* lo, int i4, float4 v) {
+// columns 4 i4 .. 4 i4 + 3 (one half of a 16-byte chunk) of rows b / B + b
+__device__ __forceinline__ void put_hilo4(__half* a, int b, int B, int n_pad, int i4, float4 v) {
   const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
   const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
-  reinterpret_cast<__half2*>(hi)[2 * i4] = h0;
-  reinterpret_cast<__half2*>(hi)[2 * i4 + 1] = h1;
-  reinterpret_cast<__half2*>(lo)[2 * i4] = __floats2half2_rn(v.x - f0.x, v.y - f0.y);
-  reinterpret_cast<__half2*>(lo)[2 * i4 + 1] = __floats2half2_rn(v.z - f1.x, v.w - f1.y);
+  __half2* hi = reinterpret_cast<__half2*>(a + ablk(b, 4 * i4, n_pad));
+  __half2* lo = reinterpret_cast<__half2*>(a + ablk(B + b, 4 * i4, n_pad));
+  hi[0] = h0;
+  hi[1] = h1;
+  lo[0] = __floats2half2_rn(v.x - f0.x, v.y - f0.y);
+  lo[1] = __floats2half2_rn(v.z - f1.x, v.w - f1.y);
 }
 __global__ void __launch_bounds__(256) ln_hilo_kernel(const float* x, int B, int h, float eps, const float* g1,
                                                       const float* b1, const float* g2, const float* b2, __half* a1,
-                                                      __half* a2) {
+                                                      __half* a2, int n_pad) {
   __shared__ float sh[32];
+  griddep_wait();
+  griddep_launch();
   const int b = blockIdx.x, h4 = h >> 2;
   const float* xb = x + (size_t)b * h;
   float4 v[4], G1[4], B1[4], G2[4], B2[4];
@@ -102,29 +116,30 @@ __global__ void __launch_bounds__(256) ln_hilo_kernel(const float* x, int B, int
     if (i4 >= h4) continue;
     const float4 n = make_float4((v[k].x - mu) * rstd, (v[k].y - mu) * rstd, (v[k].z - mu) * rstd,
                                  (v[k].w - mu) * rstd);
-    put_hilo4(a1 + (size_t)b * h, a1 + (size_t)(B + b) * h, i4,
+    put_hilo4(a1, b, B, n_pad, i4,
               make_float4(n.x * G1[k].x + B1[k].x, n.y * G1[k].y + B1[k].y, n.z * G1[k].z + B1[k].z,
                           n.w * G1[k].w + B1[k].w));
     if (a2)
-      put_hilo4(a2 + (size_t)b * h, a2 + (size_t)(B + b) * h, i4,
+      put_hilo4(a2, b, B, n_pad, i4,
                 make_float4(n.x * G2[k].x + B2[k].x, n.y * G2[k].y + B2[k].y, n.z * G2[k].z + B2[k].z,
                             n.w * G2[k].w + B2[k].w));
   }
 }
 
-// grid (B, H); y [2B][3h] (hi / lo GEMM rows) -> q [B][H][d] fp32 (rotated);
+// grid (B, H); y = the QKV GEMM (hi / lo rows) -> q [B][H][d] fp32 (rotated);
 // rotated k and v appended at `pos` of kc / vc [B][H][max_seq][d].
-__global__ void attn_prep_kernel(const float* y, int B, int H, int d, int rd, const int* state, int max_seq,
+__global__ void attn_prep_kernel(const UOut y, int B, int H, int d, int rd, const int* state, int max_seq,
                                  const float* bqkv, const float2* rope, float* q, __half* kc, __half* vc,
                                  int pos_step, size_t seq_stride) {
+  griddep_wait();
+  griddep_launch();
   // row b: position state[0] + b * pos_step (batch: 0, prefill: 1) of the
   // cache at kc + b * seq_stride (batch: own cache, prefill: the one cache)
   const int b = blockIdx.x, hh = blockIdx.y, h3 = 3 * H * d, pos = state[0] + b * pos_step;
-  const float* yh = y + (size_t)b * h3 + (size_t)hh * 3 * d;
-  const float* yl = y + (size_t)(B + b) * h3 + (size_t)hh * 3 * d;
   const float* bb = bqkv + (size_t)hh * 3 * d;
   extern __shared__ float sy[];  // [3d]
-  for (int i = threadIdx.x; i < 3 * d; i += blockDim.x) sy[i] = yh[i] + yl[i] + bb[i];
+  (void)h3;
+  for (int i = threadIdx.x; i < 3 * d; i += blockDim.x) sy[i] = uout2(y, b, B, hh * 3 * d + i) + bb[i];
   __syncthreads();
   const int half = rd >> 1;
   const float2* cs = rope + (size_t)pos * half;
@@ -159,6 +174,7 @@ __global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __
                                                         int H, int d, int max_seq, const int* state,
                                                         float scale_log2, float* part, int pos_step,
                                                         size_t seq_stride) {
+  griddep_wait();  // (no early release: this grid has many waves)
   const int bh = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
   const int P = state[0] + (bh / H) * pos_step + 1, p0 = s * kTile, n = min(kTile, P - p0);
   float* out = part + ((size_t)bh * gridDim.y + s) * (d + 2);
@@ -245,11 +261,13 @@ __global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __
 size_t attn_tile_smem(int d) { return (size_t)2 * kTile * d * 2 + (size_t)(d + kTile + 32 + 16 * d + 2) * 4 + 8; }
 
 // grid B * H, block 128: merge the S split states in split order -> ctx
-// [2B][h] fp16 hi / lo.  All states are read in one round (thread s < S
-// fetches state s), then each context element sums its S terms.
-__global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx) {
+// [2B][h] fp16 hi / lo (blocked).  All states are read in one round (thread
+// s < S fetches state s), then each context element sums its S terms.
+__global__ void attn_combine_kernel(const float* part, int S, int B, int H, int d, __half* ctx, int n_pad) {
   __shared__ float sw[256], sh[32];
-  const int bh = blockIdx.x, b = bh / H, hh = bh % H, h = H * d, tid = threadIdx.x;
+  griddep_wait();
+  griddep_launch();
+  const int bh = blockIdx.x, b = bh / H, hh = bh % H, tid = threadIdx.x;
   const float* pb = part + (size_t)bh * S * (d + 2);
   float ms = -INFINITY;
   for (int s = tid; s < S; s += blockDim.x) {
@@ -271,7 +289,7 @@ __global__ void attn_combine_kernel(const float* part, int S, int B, int H, int 
     float o = 0.f;
 #pragma unroll 8
     for (int s = 0; s < S; ++s) o += sw[s] == 0.f ? 0.f : pb[s * (d + 2) + j] * sw[s];
-    put_hilo(ctx + (size_t)b * h, ctx + (size_t)(B + b) * h, hh * d + j, o / L);
+    put_hilo(ctx, b, B, n_pad, hh * d + j, o / L);
   }
 }
 
@@ -281,86 +299,84 @@ __device__ __forceinline__ float gelu_f(float x, int exact) {
   return 0.5f * x * (1.0f + tanhf(k * fmaf(0.044715f * x, x * x, x)));
 }
 
-// grid (B, ceil(m / 256)); u [2B][m] -> g [2B][m] fp16 hi / lo
-__global__ void gelu_hilo_kernel(const float* u, int B, int m, const float* bup, int exact, __half* g) {
+// grid (B, ceil(m / 256)); u = the up GEMM (hi / lo rows) -> g hi / lo (blocked)
+__global__ void gelu_hilo_kernel(const UOut u, int B, int m, const float* bup, int exact, __half* g, int n_pad) {
+  griddep_wait();
+  griddep_launch();
   const int b = blockIdx.x, i = blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  const float v = u[(size_t)b * m + i] + u[(size_t)(B + b) * m + i] + bup[i];
-  put_hilo(g + (size_t)b * m, g + (size_t)(B + b) * m, i, gelu_f(v, exact));
+  const float v = uout2(u, b, B, i) + bup[i];
+  put_hilo(g, b, B, n_pad, i, gelu_f(v, exact));
 }
 
-// grid (B, ceil(h / 256)); x += z_hi + z_lo + b_o + dn_hi + dn_lo + b_down
-__global__ void residual_kernel(float* x, int B, int h, const float* z, const float* bo, const float* dn,
+// grid (B, ceil(h / 256)); x += W_o ctx + b_o + W_down g + b_down (z, dn: GEMMs)
+__global__ void residual_kernel(float* x, int B, int h, const UOut z, const float* bo, const UOut dn,
                                 const float* bd) {
+  griddep_wait();
+  griddep_launch();
   const int b = blockIdx.x, i = blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= h) return;
-  x[(size_t)b * h + i] += (z[(size_t)b * h + i] + z[(size_t)(B + b) * h + i] + bo[i]) +
-                          (dn[(size_t)b * h + i] + dn[(size_t)(B + b) * h + i] + bd[i]);
+  x[(size_t)b * h + i] += (uout2(z, b, B, i) + bo[i]) + (uout2(dn, b, B, i) + bd[i]);
 }
 
-// grid B: logits [2B][V] (hi / lo rows) -> argmax (lowest index on ties)
-__global__ void argmax_kernel(const float* lg, int B, int V, int* tokens, float* logits_out) {
-  __shared__ float sv[1024];
-  __shared__ int si[1024];
-  const int b = blockIdx.x;
-  float best = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = lg[(size_t)b * V + i] + lg[(size_t)(B + b) * V + i];
+// grid (B, chunks), block 256: logits (LM GEMM, hi / lo rows) -> per-block
+// argmax over a vocab chunk -> packed 64-bit atomicMax of (ordered logit,
+// ~index) into amax[b], so ties go to the lowest index like np.argmax
+// (nf/fidelity.py:27-34).  advance_kernel turns amax into tokens.
+__device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)u << 32) | (unsigned long long)(0xffffffffu - (uint32_t)idx);
+}
+__global__ void __launch_bounds__(256) argmax_kernel(const UOut lg, int B, int V, unsigned long long* amax,
+                                                     float* logits_out) {
+  __shared__ unsigned long long sb[8];
+  griddep_wait();
+  griddep_launch();
+  const int b = blockIdx.x, chunk = (V + gridDim.y - 1) / gridDim.y;
+  const int i0 = blockIdx.y * chunk, i1 = min(V, i0 + chunk);
+  unsigned long long best = 0ull;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const float v = uout2(lg, b, B, i);
     if (logits_out) logits_out[(size_t)b * V + i] = v;
-    if (v > best || (v == best && i < bi)) {
-      best = v;
-      bi = i;
-    }
+    const unsigned long long k = pack_argmax(v, i);
+    best = k > best ? k : best;
   }
-  sv[threadIdx.x] = best;
-  si[threadIdx.x] = bi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) sb[threadIdx.x >> 5] = best;
   __syncthreads();
-  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const float v = sv[threadIdx.x + s];
-      const int j = si[threadIdx.x + s];
-      if (v > sv[threadIdx.x] || (v == sv[threadIdx.x] && j < si[threadIdx.x])) {
-        sv[threadIdx.x] = v;
-        si[threadIdx.x] = j;
-      }
-    }
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = sb[w] > best ? sb[w] : best;
+    atomicMax(amax + b, best);
   }
-  if (threadIdx.x == 0) tokens[b] = si[0];
 }
 
 // grid B: x[b] = embed[token[b]]
 __global__ void embed_kernel(const int* tokens, const __half* embed, int h, int V, float* x) {
+  griddep_wait();
+  griddep_launch();
   const int b = blockIdx.x;
   int t = tokens[b];
   t = (t < 0 || t >= V) ? 0 : t;
   for (int i = threadIdx.x; i < h; i += blockDim.x) x[(size_t)b * h + i] = __half2float(embed[(size_t)t * h + i]);
 }
 
-__global__ void advance_pos_kernel(int* state) { state[0] += 1; }
-
-}  // namespace nfb
-
-namespace nfb {
-
-// out[c][r] = in[r][c] (fp16, rows x cols), 32 x 32 tiles
-__global__ void transpose_f16_kernel(const __half* in, __half* out, int rows, int cols) {
-  __shared__ __half tile[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int r = r0 + i, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[i][threadIdx.x] = in[(size_t)r * cols + c];
+// End of a step: position + 1; with the head, amax -> tokens (and amax
+// cleared for the next step's atomicMax).
+__global__ void advance_kernel(int* state, unsigned long long* amax, int* tokens, int B, int V) {
+  griddep_wait();
+  griddep_launch();
+  for (int b = threadIdx.x; b < B && amax; b += blockDim.x) {
+    const unsigned long long k = amax[b];
+    int t = (int)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
+    tokens[b] = (t < 0 || t >= V) ? 0 : t;
+    amax[b] = 0ull;
   }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[(size_t)c * rows + r] = tile[threadIdx.x][i];
-  }
-}
-
-void transpose_f16(cudaStream_t st, const __half* in, __half* out, int rows, int cols) {
-  transpose_f16_kernel<<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, st>>>(in, out, rows, cols);
+  if (threadIdx.x == 0) state[0] += 1;
 }
 
 }  // namespace nfb

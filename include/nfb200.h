@@ -16,6 +16,7 @@
 #ifndef NFB200_H
 #define NFB200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -209,13 +210,25 @@ int nfb_batch_read_tokens(nfb_ctx* ctx, int* tokens);
  * hold exactly `pos` positions), final hidden states to x_out (optional).
  * Runs on the batched kernels in chunks of max_batch rows (nfb_batch_init). */
 int nfb_prefill(nfb_ctx* ctx, int pos, int count, const float* x_in, float* x_out);
-/* Diagnostics: the batched-projection GEMM (csrc/nfb_umma.cu, tcgen05 + TMA,
- * stream-K with a deterministic fixup) on caller-owned DEVICE buffers:
- * Y[N][M] (fp32) = W[M][K] (fp16, row-major) . A[N][K]^T (fp16), N <= 256,
- * K % 8 == 0, enqueued on `stream` (NULL = legacy default).  Not in the
- * reference; used by the unit test / microbenchmark of that kernel.  Returns 0
- * or a negative code.  Not thread-safe (one shared workspace). */
+/* Diagnostics: the batched-projection GEMM (csrc/nfb_umma.cu: tcgen05 + TMEM,
+ * weights pre-blocked into the UMMA SW128 layout and streamed with 1-D bulk
+ * copies, stream-K partials summed in piece order) on caller-owned DEVICE
+ * buffers: Y[N][M] (fp32) = W[M][K] (fp16, row-major) . A[N][K]^T (fp16),
+ * N <= 256, enqueued on `stream` (NULL = legacy default).  Not in the
+ * reference; used by the unit test / microbenchmark of that kernel.  Return 0
+ * or a negative code.  Not thread-safe (one shared workspace).
+ *   nfb_gemm_f16_dev          blocks W into the workspace, then runs;
+ *   nfb_gemm_blocked_bytes    size of the blocked copy of an M x K matrix;
+ *   nfb_gemm_block_weights_dev  W (row-major) -> Wb (blocked), on `stream`;
+ *   nfb_gemm_f16_blocked_dev  runs on a pre-blocked Wb (the batched path's
+ *                             steady state: weights blocked once). */
 int nfb_gemm_f16_dev(int M, int N, int K, const void* W, const void* A, float* Y, void* stream);
+size_t nfb_gemm_blocked_bytes(int M, int K);
+int nfb_gemm_block_weights_dev(int M, int K, const void* W, void* Wb, void* stream);
+int nfb_gemm_f16_blocked_dev(int M, int N, int K, const void* Wb, const void* A, float* Y, void* stream);
+/* Diagnostics: per-CTA globaltimer stamps ([grid][8] u64, caller-owned device
+ * buffer; NULL turns it off) of the following standalone GEMM launches. */
+int nfb_gemm_trace_dev(void* buf);
 
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);

@@ -69,6 +69,10 @@ SIGNATURES = {
     "nfb_forward": (_I, [_P, _I, _FP, _FP, _FP, _I]),
     "nfb_block_step_dev": (_I, [_P, _I, _I, _P, _P, _P]),
     "nfb_gemm_f16_dev": (_I, [_I, _I, _I, _P, _P, _P, _P]),
+    "nfb_gemm_blocked_bytes": (C.c_size_t, [_I, _I]),
+    "nfb_gemm_block_weights_dev": (_I, [_I, _I, _P, _P, _P]),
+    "nfb_gemm_f16_blocked_dev": (_I, [_I, _I, _I, _P, _P, _P, _P]),
+    "nfb_gemm_trace_dev": (_I, [_P]),
     "nfb_forward_dev": (_I, [_P, _I, _P, _P, _P, _I, _P]),
     "nfb_begin_decode": (_I, [_P, _I, _I]),
     "nfb_decode_step": (_I, [_P, _P]),

@@ -50,3 +50,26 @@ def test_umma_gemm_is_deterministic():
     W = (rng.uniform(-1, 1, (2560, 10240)) / 100).astype(np.float16)
     A = rng.standard_normal((128, 10240)).astype(np.float16)
     assert np.array_equal(gemm(W, A), gemm(W, A))
+
+
+def test_preblocked_weights_entry_matches():
+    """The steady-state entry (weights blocked once into the UMMA SW128 layout,
+    csrc/nfb_umma.cuh) gives the same bits as block-then-run."""
+    import torch
+    from paper_2604_23553_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(11)
+    M, N, K = 2560, 32, 10240
+    W = (rng.uniform(-1, 1, (M, K)) / 100).astype(np.float16)
+    A = rng.standard_normal((N, K)).astype(np.float16)
+    Wd = torch.from_numpy(W).cuda()
+    Ad = torch.from_numpy(A).cuda()
+    Wb = torch.empty(lib.nfb_gemm_blocked_bytes(M, K) // 2, dtype=torch.float16, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.nfb_gemm_block_weights_dev(M, K, C.c_void_p(Wd.data_ptr()), C.c_void_p(Wb.data_ptr()),
+                                          C.c_void_p(st)) == 0
+    Y = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    assert lib.nfb_gemm_f16_blocked_dev(M, N, K, C.c_void_p(Wb.data_ptr()), C.c_void_p(Ad.data_ptr()),
+                                        C.c_void_p(Y.data_ptr()), C.c_void_p(st)) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.cpu().numpy(), gemm(W, A))

@@ -1,7 +1,7 @@
 # quick GPU check: parity tests + bench + trace (+ optional debug modes)
 set -u
 TAG=${1:-q}; OUT=gpurun_out/$TAG; mkdir -p $OUT
-timeout 600 python -m pytest tests -x -q -m gpu > $OUT/pytest.log 2>&1; echo "pytest: $(tail -1 $OUT/pytest.log)"
+[ -n "${NO_TEST:-}" ] || timeout 600 python -m pytest tests -x -q -m gpu > $OUT/pytest.log 2>&1; echo "pytest: $(tail -1 $OUT/pytest.log)"
 timeout 300 python bench.py --steps 64 --warmup 5 --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err
 echo "bench: $(python -c "import json;d=json.load(open('$OUT/bench.json'));print(round(d['value'],1), round(d['ms_per_step']*1000,1),'us', round(d['roofline']['frac'],3), d['clocks'])" 2>&1 | tail -1)"
 timeout 120 python tools/trace_decode.py --out $OUT/trace.json > $OUT/trace.log 2>&1
