@@ -336,6 +336,8 @@ struct nfb_ctx {
   int pf_ahead = 0;  // L2 prefetcher lead (bytes); measured: no gain at C2
   int mlp_gap = 1;   // MLP pairs interleaved into the head schedule (split-phase cluster syncs)
   int fold_all = 1;  // see Params::fold_all
+  int deterministic = 0;  // 1: fixed-order fold layer end (bitwise reproducible) instead of fp32 atomics
+  float* acc = nullptr;   // [n_layers][hidden] atomic layer-end accumulators
   int pair = 7;      // consumer stage pairing mask (1 MLP, 2 QKV, 4 W_out)
   unsigned long long* h_tok = nullptr;  // pinned [2]
   std::vector<void*> allocs;
@@ -430,6 +432,8 @@ Params base_params(nfb_ctx* c) {
   p.mlp_gap = c->mlp_gap;
   p.pair = (c->dpl & 1) ? (c->pair & 1) : c->pair;  // two-chunk variant: MLP pairs only (compiled out)
   p.fold_all = c->fold_all;
+  p.acc = c->acc;
+  p.acc_mode = (m.parallel_residual && c->tp_size == 1 && !c->deterministic) ? 1 : 0;
   p.tp_root = c->tp_rank == 0 ? 1 : 0;
   p.state_update = 1;
   p.vocab_offset = c->tp_rank * c->desc.vocab;
@@ -501,6 +505,9 @@ namespace {
 // parity slot exhausted by an earlier launch hands out no rows.
 int reset_counters(nfb_ctx* c, cudaStream_t st) {
   CK(cudaMemsetAsync(c->ctr, 0, sizeof(int) * 2 * (size_t)c->ctr_stride, st));
+  // the atomic layer-end accumulators are all zero between launches (the
+  // kernel re-zeroes them); re-establish that after a rewind or a fault
+  CK(cudaMemsetAsync(c->acc, 0, sizeof(float) * (size_t)c->desc.n_layers * c->desc.hidden, st));
   return NFB_OK;
 }
 
@@ -676,6 +683,7 @@ static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, in
   if (c->dpl & 1) c->pair = 1;
   if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
   if (getenv("NFB_FOLD_ALL")) c->fold_all = atoi(getenv("NFB_FOLD_ALL")) ? 1 : 0;
+  if (getenv("NFB_DETERMINISTIC")) c->deterministic = atoi(getenv("NFB_DETERMINISTIC")) ? 1 : 0;
   if (getenv("NFB_ASSIST")) c->assist = atoi(getenv("NFB_ASSIST"));
   if (getenv("NFB_DYN_MLP")) c->dyn_mlp = atoi(getenv("NFB_DYN_MLP")) ? 1 : 0;
   // assist needs CTAs without heads, parts of a multiple of 4 rows, <= 8 parts
@@ -720,7 +728,8 @@ static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, in
       (r = dalloc(c, &c->unembed, (size_t)V * h)) || (r = dalloc(c, &c->lnfg, h)) ||
       (r = dalloc(c, &c->lnfb, h)) || (r = dalloc(c, &c->rope, (size_t)max_seq * (m.rotary_dims / 2))) ||
       (r = dalloc(c, &c->xs, (size_t)(L + 1) * h)) || (r = dalloc(c, &c->rbuf, h)) ||
-      (r = dalloc(c, &c->part, (size_t)nc * C * h)) || (r = dalloc(c, &c->logits, V)) ||
+      (r = dalloc(c, &c->part, (size_t)nc * C * h)) || (r = dalloc(c, &c->acc, (size_t)L * h)) ||
+      (r = dalloc(c, &c->logits, V)) ||
       (r = dalloc(c, &c->ctr, 2 * c->ctr_stride)) || (r = dalloc(c, &c->gbar, 2)) ||
       (r = dalloc(c, &c->state, 2)) || (r = dalloc(c, &c->amax, 2)) ||
       (r = dalloc(c, &c->tokens, max_seq)) || (r = dalloc(c, &c->err, 1)) ||
@@ -1317,6 +1326,8 @@ int nfb_set_option(nfb_ctx* c, int option, int value) {
     if (value && (value > 6 || d3 % (C + value) || (d3 / (C + value)) % 4 || c->grid <= C * std::min(c->desc.n_heads, c->n_clusters)))
       return fail(NFB_EUNSUPPORTED, "QKV assist needs CTAs without heads and parts of a multiple of 4 rows");
     c->assist = value;
+  } else if (option == NFB_OPT_DETERMINISTIC) {
+    c->deterministic = value ? 1 : 0;
   } else if (option == NFB_OPT_PREFETCH_KB) {
     if (value < 0 || value > 65536) return fail(NFB_EINVAL, "prefetch lead must be in [0, 65536] KiB");
     c->pf_ahead = value * 1024;

@@ -596,9 +596,15 @@ struct Consumer {
     if (lane == 0) mbar_arrive_u32(empty_s + 8u * sl);
   }
 
-  // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40)
+  // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40);
+  // statistics once per vector (LN1 and LN2 of the parallel residual share them)
   __device__ __forceinline__ void layer_norm(const float (&x)[NCH][8], const float* g, const float* b,
                                              float2 (&out)[NCH][4]) {
+    float mu, rstd;
+    ln_stats(x, mu, rstd);
+    ln_apply(x, mu, rstd, g, b, out);
+  }
+  __device__ __forceinline__ void ln_stats(const float (&x)[NCH][8], float& mu_out, float& rstd_out) {
     float sm = 0.f;
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
@@ -613,7 +619,11 @@ struct Consumer {
 #pragma unroll
         for (int i = 0; i < 8; ++i) sq += (x[k][i] - mu) * (x[k][i] - mu);
     const float var = consumer_sum(sq, reinterpret_cast<float*>(s.misc) + 32, p.ncw, warp, lane) / p.h;
-    const float rstd = rsqrtf(var + p.eps);
+    mu_out = mu;
+    rstd_out = rsqrtf(var + p.eps);
+  }
+  __device__ __forceinline__ void ln_apply(const float (&x)[NCH][8], float mu, float rstd, const float* g,
+                                           const float* b, float2 (&out)[NCH][4]) {
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
       if (act[k]) {
@@ -1041,8 +1051,12 @@ struct Consumer {
 
   // ---- layer-end reduction -------------------------------------------------
   // event 0: parallel END, 1: sequential SYNC (attention half), 2: sequential END
-  __device__ __forceinline__ void reduce_event(int event, int lrel) {
+  __device__ __forceinline__ void reduce_event(int event, int lrel, const float (&xin_r)[NCH][8]) {
     const int h = p.h;
+    if (p.acc_mode && event == 0) {
+      acc_layer_end(lrel, xin_r);
+      return;
+    }
     // 1) split-K partials of the cluster -> rank 0 via DSMEM (fold_all: every
     //    CTA publishes its own partial and the fold sums G of them instead)
     if (p.C > 1 && !p.fold_all) {
@@ -1200,6 +1214,90 @@ struct Consumer {
       for (int i = 0; i < 4; ++i) acc2[k][i] = make_float2(0.f, 0.f);
   }
 
+  // ---- atomic layer end (acc_mode, parallel residual) ----------------------
+  // Every CTA adds its split-K partial into acc[lrel] with vector fp32
+  // reductions (CTA 0 also adds the residual input and b_o + b_down), then ONE
+  // grid barrier; afterwards acc[lrel] is the next layer's input.  Replaces
+  // store-partials / barrier / fixed-order fold / barrier.  fp32 addition
+  // order across CTAs varies run to run (~1e-7 relative): not bitwise
+  // reproducible -- the deterministic fold stays available (NFB_OPT_DETERMINISTIC).
+  // Each chunk c has an owner CTA (c % grid) that, after the barrier, copies
+  // acc[lrel] chunk c to xs[lrel + 1] (layer outputs for readers outside the
+  // kernel) and zeroes acc[lrel - 1] chunk c (everyone has read it by now), so
+  // the accumulators are all zero again between launches (the last one is
+  // zeroed after the head, see run()).
+  unsigned long long acc_target = 0;
+  __device__ __forceinline__ void acc_layer_end(int lrel, const float (&xin_r)[NCH][8]) {
+    const int h = p.h, G = gridDim.x;
+    const LayerW& W = s.lw[lrel & 1];
+    if (blockIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NCH; ++k)
+        if (act[k]) {
+          const float4 bo0 = __ldg(reinterpret_cast<const float4*>(W.bo) + 2 * col[k]);
+          const float4 bo1 = __ldg(reinterpret_cast<const float4*>(W.bo) + 2 * col[k] + 1);
+          const float4 bd0 = __ldg(reinterpret_cast<const float4*>(W.bd) + 2 * col[k]);
+          const float4 bd1 = __ldg(reinterpret_cast<const float4*>(W.bd) + 2 * col[k] + 1);
+          const float bb[8] = {bo0.x + bd0.x, bo0.y + bd0.y, bo0.z + bd0.z, bo0.w + bd0.w,
+                               bo1.x + bd1.x, bo1.y + bd1.y, bo1.z + bd1.z, bo1.w + bd1.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            acc2[k][i].x += xin_r[k][2 * i] + bb[2 * i];
+            acc2[k][i].y += xin_r[k][2 * i + 1] + bb[2 * i + 1];
+          }
+        }
+    }
+    float* dst = p.acc + (size_t)lrel * h;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (act[k]) {
+        red_add_v4(dst + col[k] * 8, acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y);
+        red_add_v4(dst + col[k] * 8 + 4, acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y);
+      }
+    if (tid < (int)(sizeof(LayerW) / 8) && cur_layer + 1 < p.l1)
+      reinterpret_cast<unsigned long long*>(&s.lw[(lrel + 1) & 1])[tid] =
+          reinterpret_cast<const unsigned long long*>(&p.layers[cur_layer + 1])[tid];
+    consumer_sync(nct);
+    stamp_layer(lrel, 8);
+    if (tid == 0) {
+      grid_sync(p.gbar, gridDim.x, p.err);
+      if (blockIdx.x == 0 && n_events == 0) *p.epoch = epoch_base + (unsigned)(p.l1 - p.l0);
+      if (blockIdx.x == 0 && n_events == 0 && p.state_update) {
+        p.state[0] = pos + (p.advance_pos ? 1 : 0);
+        p.state[1] = step + 1;
+      }
+    }
+    ++n_events;
+    consumer_sync(nct);
+    stamp_layer(lrel, 4);
+    const bool last_no_head = (lrel + 1 == p.l1 - p.l0) && p.head_mode == HEAD_NONE;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (act[k] && col[k] % G == (int)blockIdx.x) {
+        const float4* src = reinterpret_cast<const float4*>(dst + col[k] * 8);
+        const float4 a = __ldcg(src), b = __ldcg(src + 1);
+        float4* xo = reinterpret_cast<float4*>(p.xs + (size_t)(lrel + 1) * h + col[k] * 8);
+        xo[0] = a;
+        xo[1] = b;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lrel > 0) {
+          float4* zp = reinterpret_cast<float4*>(p.acc + (size_t)(lrel - 1) * h + col[k] * 8);
+          zp[0] = z;
+          zp[1] = z;
+        }
+        if (last_no_head) {  // nobody else reads the last accumulator
+          float4* zp = reinterpret_cast<float4*>(dst + col[k] * 8);
+          zp[0] = z;
+          zp[1] = z;
+        }
+      }
+    stamp_layer(lrel, 5);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc2[k][i] = make_float2(0.f, 0.f);
+  }
+
   // ---- main loop --------------------------------------------------------------
   __device__ __forceinline__ void run() {
     const int h = p.h;
@@ -1228,7 +1326,8 @@ struct Consumer {
           }
         }
       } else {
-        load_vec(p.xs + (size_t)lrel * h, x);
+        // atomic layer end: the previous layer's sum is complete in acc[lrel - 1]
+        load_vec((p.acc_mode && lrel > 0) ? p.acc + (size_t)(lrel - 1) * h : p.xs + (size_t)lrel * h, x);
       }
       // this CTA's up biases (static MLP range) -> smem; read at the FLUSH
       // points after a consumer barrier (the first one follows the LNs)
@@ -1237,8 +1336,12 @@ struct Consumer {
         ubn = min(min(s.misc[4] * p.stage_rows, p.m) - ub0, kMaxBias);
         for (int i = tid; i < ubn; i += nct) s.ubias[i] = __ldg(W.bup + ub0 + i);
       }
-      layer_norm(x, W.ln1g, W.ln1b, xn1);
-      if (p.parallel) layer_norm(x, W.ln2g, W.ln2b, xn2);
+      {
+        float mu, rstd;
+        ln_stats(x, mu, rstd);
+        ln_apply(x, mu, rstd, W.ln1g, W.ln1b, xn1);
+        if (p.parallel) ln_apply(x, mu, rstd, W.ln2g, W.ln2b, xn2);
+      }
       stamp_layer(lrel, 0);
 #pragma unroll
       for (int k = 0; k < NCH; ++k)
@@ -1402,7 +1505,7 @@ struct Consumer {
           release(sl);
           qkv_complete();
           attention_complete();
-          reduce_event(1, lrel);
+          reduce_event(1, lrel, x);
           float r[NCH][8];
           load_vec(p.rbuf, r);
           layer_norm(r, W.ln2g, W.ln2b, xn2);
@@ -1411,7 +1514,7 @@ struct Consumer {
           qkv_complete();
           attention_complete();
           stamp_layer(lrel, 3);
-          reduce_event(p.parallel ? 0 : 2, lrel);
+          reduce_event(p.parallel ? 0 : 2, lrel, x);
           break;
         } else {
           // unexpected stage type: poison and stop
@@ -1420,7 +1523,23 @@ struct Consumer {
         if (slog) slog[2] = clock64();
       }
     }
-    if (p.head_mode != HEAD_NONE) run_head();
+    if (p.head_mode != HEAD_NONE) {
+      run_head();
+      if (p.acc_mode && p.l1 > p.l0) {
+        // every CTA read the last accumulator at the head's start (and
+        // arrived then): zero this CTA's chunks of it once all have
+        if (tid == 0) grid_wait(p.gbar, acc_target, p.err);
+        consumer_sync(nct);
+        const int L = p.l1 - p.l0;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          if (act[k] && col[k] % (int)gridDim.x == (int)blockIdx.x) {
+            float4* zp = reinterpret_cast<float4*>(p.acc + (size_t)(L - 1) * h + col[k] * 8);
+            zp[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            zp[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+      }
+    }
     stamp(3);
     if ((TR && p.trace != nullptr) && tid == 0) {
       p.trace[(size_t)blockIdx.x * p.trace_stride + 1] = wait_ns;
@@ -1434,7 +1553,12 @@ struct Consumer {
     stamp(4);
     const int L = p.l1 - p.l0;
     float x[NCH][8];
-    load_vec(p.xs + (size_t)L * h, x);
+    const bool from_acc = p.acc_mode && L > 0;
+    load_vec(from_acc ? p.acc + (size_t)(L - 1) * h : p.xs + (size_t)L * h, x);
+    if (from_acc) {
+      consumer_sync(nct);  // all of this CTA's reads of the accumulator are done
+      if (tid == 0) acc_target = grid_arrive(p.gbar, gridDim.x);
+    }
     if (p.head_mode == HEAD_LM) {
       layer_norm(x, p.head.lnfg, p.head.lnfb, xn1);
     } else {

@@ -91,6 +91,8 @@ struct Params {
   float* xs;            // [(l1-l0)+1][h] hidden states (xs[0] = block input)
   float* rbuf;          // [h] sequential-residual temp
   float* part;          // [n_clusters][h] cluster partial sums
+  float* acc;           // [layers][h] atomic split-K accumulators (acc_mode), all zero between launches
+  int acc_mode;         // 1: layer end = red.add.v4.f32 of every CTA's partial + ONE grid barrier
   int* ctr;             // [2][ctr_stride] dynamic chunk counters by step parity
   int ctr_stride;
   unsigned long long* gbar;  // grid barrier arrival counter (monotonic)

@@ -208,6 +208,24 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   return v;
 }
 
+// Split-phase grid barrier: arrive now, wait for `target` later.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* bar, unsigned nblocks) {
+  const unsigned long long old = atom_add_acqrel_u64(bar, 1ull);
+  return (old / nblocks + 1ull) * nblocks;
+}
+__device__ __forceinline__ void grid_wait(unsigned long long* bar, unsigned long long target, int* err) {
+  if (ld_acquire_u64(bar) >= target) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_u64(bar) < target) {
+    if (globaltimer() - t0 > kTimeoutNs) fail_timeout(err, 3);
+  }
+}
+
+// Vector fp32 reduction into global memory (sm_90+), 16-byte aligned.
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 __device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned nblocks, int* err) {
   const unsigned long long old = atom_add_acqrel_u64(bar, 1ull);
   const unsigned long long target = (old / nblocks + 1ull) * nblocks;

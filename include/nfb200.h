@@ -159,6 +159,8 @@ int nfb_get_state(nfb_ctx* ctx, int* pos, int* step);
 #define NFB_OPT_PREFETCH_KB 3 /* L2 prefetch lead of the prefetcher warp, KiB (0 = off) */
 #define NFB_OPT_HEAD_WEIGHT 4 /* static MLP split: head bytes weighted by value / 100 (default 130) */
 #define NFB_OPT_ASSIST 5      /* QKV parts per head computed by CTAs without heads (0 = off) */
+#define NFB_OPT_DETERMINISTIC 6 /* 1: fixed-order fold at each layer end (bitwise reproducible run to run);
+                                 * 0 (default): fp32 vector atomics + one grid barrier per layer */
 int nfb_set_option(nfb_ctx* ctx, int option, int value);
 /* Copy up to n trace words ([grid][8 + 12*n_layers]) to `out`. */
 int nfb_read_trace(nfb_ctx* ctx, unsigned long long* out, int n);

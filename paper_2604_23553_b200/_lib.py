@@ -17,7 +17,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "nfb200.h")
 NFB_OK, NFB_EINVAL, NFB_ECUDA, NFB_ESTATE, NFB_EUNSUPPORTED, NFB_EDEVICE = 0, -1, -2, -3, -4, -5
 NFB_F64, NFB_F32, NFB_F16 = 0, 1, 2
 HEAD_NONE, HEAD_PROBE, HEAD_LM = 0, 1, 2
-OPT_TRACE, OPT_DYNAMIC_MLP, OPT_PREFETCH_KB, OPT_HEAD_WEIGHT, OPT_ASSIST = 1, 2, 3, 4, 5
+OPT_TRACE, OPT_DYNAMIC_MLP, OPT_PREFETCH_KB, OPT_HEAD_WEIGHT, OPT_ASSIST, OPT_DETERMINISTIC = 1, 2, 3, 4, 5, 6
 
 
 class ModelDesc(C.Structure):

@@ -298,10 +298,12 @@ class Engine:
 
     def set_option(self, option: str, value) -> None:
         """"trace" / "dynamic_mlp" (bool), "prefetch_kb" (L2 prefetch lead, KiB),
-        "head_weight" (static MLP split, percent) or "assist" (QKV assist parts)."""
+        "head_weight" (static MLP split, percent), "assist" (QKV assist parts) or
+        "deterministic" (bool: fixed-order fold at each layer end, bitwise
+        reproducible; default off = fp32 vector atomics, one barrier per layer)."""
         code = {"trace": _lib.OPT_TRACE, "dynamic_mlp": _lib.OPT_DYNAMIC_MLP,
                 "prefetch_kb": _lib.OPT_PREFETCH_KB, "head_weight": _lib.OPT_HEAD_WEIGHT,
-                "assist": _lib.OPT_ASSIST}[option]
+                "assist": _lib.OPT_ASSIST, "deterministic": _lib.OPT_DETERMINISTIC}[option]
         v = int(value) if option in ("prefetch_kb", "head_weight", "assist") else int(bool(value))
         check(self.lib.nfb_set_option(self._h, code, v), "nfb_set_option")
 
