@@ -442,8 +442,14 @@ Params base_params(nfb_ctx* c) {
   return p;
 }
 
+// The lean production kernel variant has only the default path; tracing,
+// debug modes and the experimental options run on the full variant.
+bool needs_full_variant(const nfb_ctx* c) {
+  return c->trace || c->debug || c->assist || c->pf_ahead > 0 || c->dyn_mlp || !c->fold_all;
+}
+
 int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {
-  const int variant = c->dpl + ((c->trace || c->debug) ? 2 : 0);
+  const int variant = c->dpl + (needs_full_variant(c) ? 2 : 0);
   cudaError_t e = launch_decode(p, variant, c->grid, c->block, c->smem, st, c->coop);
   if (e != cudaSuccess && c->coop) {
     // Cooperative + cluster launch refused: fall back to the occupancy-checked
@@ -1247,7 +1253,7 @@ int nfb_graph_capture(nfb_ctx* c) {
     return NFB_OK;
   }
   const Params p = decode_params(c);
-  const int variant = c->dpl + ((c->trace || c->debug) ? 2 : 0);
+  const int variant = c->dpl + (needs_full_variant(c) ? 2 : 0);
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   cudaError_t e = launch_decode(p, variant, c->grid, c->block, c->smem, c->stream, c->coop);
   cudaGraph_t g = nullptr;

@@ -192,7 +192,7 @@ struct Producer {
   // against the other lanes' end-of-kernel cluster barrier); lane 0 issues.
   __device__ __forceinline__ void push(int type, int a, int n, int flags, const void* src0, uint32_t b0,
                        const void* src1 = nullptr, uint32_t b1 = 0) {
-    if (pf) {
+    if (TR && pf) {
       const uint32_t need = cum16 + ((b0 + b1) >> 4);
       const uint32_t ahead = (uint32_t)p.pf_ahead >> 4;
       while (need > *shared_cum16 + ahead) __nanosleep(256);
@@ -256,7 +256,7 @@ struct Producer {
     const uint32_t rowb = (uint32_t)p.h * 2u;
     for (int k = 0; max_pairs < 0 || k < max_pairs; ++k) {
       int ca, cb;
-      if (p.dyn_mlp) {
+      if (TR && p.dyn_mlp) {
         ca = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctr, 1) : 0, 0);
         if (ca * p.stage_rows >= p.m) break;
         cb = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctr, 1) : 0, 0);
@@ -289,14 +289,14 @@ struct Producer {
   __device__ __forceinline__ void run(int pos, int par, uint32_t rank, uint32_t cid) {
     const int h = p.h, d = p.d, C = p.C;
     const uint32_t rowb = (uint32_t)h * 2u;
-    const int gap = (p.parallel && !p.dyn_mlp) ? p.mlp_gap : 0;
+    const int gap = (p.parallel && !(TR && p.dyn_mlp)) ? p.mlp_gap : 0;
     for (int l = p.l0; l < p.l1; ++l) {
       const LayerW& W = p.layers[l];
       const int lrel = l - p.l0;
       log_on = lrel == (p.l1 - p.l0) / 2;
       int* ctr = p.ctr + par * p.ctr_stride + lrel;
       int next = mlp_c0;
-      if (p.assist) {
+      if (TR && p.assist) {
         // assist units of this CTA: QKV part (C + a) of head u / A, first thing
         const int g = (int)(cid * C + rank), G = p.n_clusters * C, f = assist_first_cta(p), G2 = G - f;
         for (int u = g - f; g >= f && u < p.H * p.assist; u += G2) {
@@ -344,11 +344,11 @@ struct Producer {
         }
       }
       if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
-      if (pf && p.dyn_mlp) return;  // dynamic chunk grabs cannot be replayed
+      if (TR && pf && p.dyn_mlp) return;  // dynamic chunk grabs cannot be replayed
       emit_mlp(W, ctr, next, -1);
       push(ST_END, 0, 0, 0, nullptr, 0);
     }
-    if (pf) return;
+    if (TR && pf) return;
     if (p.head_mode != HEAD_NONE) {
       int* ctr = p.ctr + par * p.ctr_stride + (p.l1 - p.l0);
       for (;;) {
@@ -1014,7 +1014,7 @@ struct Consumer {
     const int head = pend_head;
     long long t0 = tick();
     mbar_wait_u32(smem_u32(s.bar_qkv), n_qkv & 1, p.err, 11);
-    if (p.assist) {
+    if (TR && p.assist) {
       // the assist parts of this head: rows [C * rows_qkv, 3d) from global memory
       const unsigned want = epoch_base + (unsigned)(cur_layer - p.l0) + 1u;
       if (tid < p.assist) {
@@ -1051,15 +1051,18 @@ struct Consumer {
 
   // ---- layer-end reduction -------------------------------------------------
   // event 0: parallel END, 1: sequential SYNC (attention half), 2: sequential END
-  __device__ __forceinline__ void reduce_event(int event, int lrel, const float (&xin_r)[NCH][8]) {
+  __device__ __forceinline__ void reduce_event(int event, int lrel) {
     const int h = p.h;
     if (p.acc_mode && event == 0) {
-      acc_layer_end(lrel, xin_r);
+      acc_layer_end(lrel);
       return;
     }
     // 1) split-K partials of the cluster -> rank 0 via DSMEM (fold_all: every
     //    CTA publishes its own partial and the fold sums G of them instead)
-    if (p.C > 1 && !p.fold_all) {
+    // (production variant: fold_all only; the cluster pre-reduce is in the
+    // full / trace variant)
+    const bool fold_all = !TR || p.fold_all;
+    if (p.C > 1 && !fold_all) {
       if (rank != 0) {
         // stage the partial in this CTA's own red_in slot, then one bulk copy
         // into the same slot of rank 0 (complete_tx on rank 0's barrier)
@@ -1093,12 +1096,12 @@ struct Consumer {
       }
       ++n_red;
     }
-    const int npart = p.fold_all ? (int)gridDim.x : p.n_clusters;
-    if (rank == 0 || p.fold_all)
+    const int npart = fold_all ? (int)gridDim.x : p.n_clusters;
+    if (rank == 0 || fold_all)
 #pragma unroll
       for (int k = 0; k < NCH; ++k)
         if (act[k]) {
-          float4* dst = reinterpret_cast<float4*>(p.part + (size_t)(p.fold_all ? blockIdx.x : cid) * h + col[k] * 8);
+          float4* dst = reinterpret_cast<float4*>(p.part + (size_t)(fold_all ? blockIdx.x : cid) * h + col[k] * 8);
           __stcg(dst, make_float4(acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y));
           __stcg(dst + 1, make_float4(acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y));
         }
@@ -1227,10 +1230,22 @@ struct Consumer {
   // the accumulators are all zero again between launches (the last one is
   // zeroed after the head, see run()).
   unsigned long long acc_target = 0;
-  __device__ __forceinline__ void acc_layer_end(int lrel, const float (&xin_r)[NCH][8]) {
+  __device__ __forceinline__ void acc_layer_end(int lrel) {
     const int h = p.h, G = gridDim.x;
     const LayerW& W = s.lw[lrel & 1];
     if (blockIdx.x == 0) {
+      // the layer's residual input, re-read (not kept live in registers
+      // through the layer): the launch input / token embedding, or the
+      // previous accumulator (zeroed only after this layer's barrier)
+      float xin_r[NCH][8];
+      if (lrel == 0 && p.in_mode == IN_TOKEN) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          if (act[k]) h8_to_f32(__ldg(reinterpret_cast<const uint4*>(p.head.embed + (size_t)s.misc[2] * h) + col[k]),
+                                xin_r[k]);
+      } else {
+        load_vec(lrel == 0 ? p.xs : p.acc + (size_t)(lrel - 1) * h, xin_r);
+      }
 #pragma unroll
       for (int k = 0; k < NCH; ++k)
         if (act[k]) {
@@ -1331,7 +1346,7 @@ struct Consumer {
       }
       // this CTA's up biases (static MLP range) -> smem; read at the FLUSH
       // points after a consumer barrier (the first one follows the LNs)
-      if (!p.dyn_mlp) {
+      if (!(TR && p.dyn_mlp)) {
         ub0 = s.misc[3] * p.stage_rows;
         ubn = min(min(s.misc[4] * p.stage_rows, p.m) - ub0, kMaxBias);
         for (int i = tid; i < ubn; i += nct) s.ubias[i] = __ldg(W.bup + ub0 + i);
@@ -1411,7 +1426,7 @@ struct Consumer {
             qkv_publish(head);
             tock(13, tq);
           }
-        } else if (dsc.type == ST_AQKV) {
+        } else if (TR && dsc.type == ST_AQKV) {
           // assist part of head u / A: row-dots, then publish to global
           if (dsc.flags & F_FIRST) pend = 0;
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
@@ -1505,7 +1520,7 @@ struct Consumer {
           release(sl);
           qkv_complete();
           attention_complete();
-          reduce_event(1, lrel, x);
+          reduce_event(1, lrel);
           float r[NCH][8];
           load_vec(p.rbuf, r);
           layer_norm(r, W.ln2g, W.ln2b, xn2);
@@ -1514,7 +1529,7 @@ struct Consumer {
           qkv_complete();
           attention_complete();
           stamp_layer(lrel, 3);
-          reduce_event(p.parallel ? 0 : 2, lrel, x);
+          reduce_event(p.parallel ? 0 : 2, lrel);
           break;
         } else {
           // unexpected stage type: poison and stop
@@ -1679,7 +1694,7 @@ __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
   cluster_sync_all();
   const int pos = s.misc[0], step = s.misc[1];
 
-  if (warp == p.ncw || (warp == p.ncw + 1 && p.pf_ahead > 0)) {
+  if (warp == p.ncw || (TR && warp == p.ncw + 1 && p.pf_ahead > 0)) {
     Producer<TR> prod(p, s, tid & 31, warp != p.ncw);
     prod.mlp_c0 = s.misc[3];
     prod.mlp_c1 = s.misc[4];
@@ -1692,8 +1707,11 @@ __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
 }
 
 // Kernel variants: 1 or 2 hidden chunks per consumer thread (hidden <= 2560 /
-// <= 5120), each without / with the trace + measurement-debug paths compiled
-// in (variant = (NCH - 1) + 2 * trace).  Blocks are always <= 384 threads.
+// <= 5120), each as the lean production variant or the FULL variant (TR =
+// true: trace + measurement-debug paths and the optional experimental paths
+// -- QKV assist, L2 prefetcher warp, work-stealing MLP, cluster pre-reduce
+// fold -- compiled in; variant = (NCH - 1) + 2 * full).  Blocks are always
+// <= 384 threads.
 #define NFB_VARIANTS(X) X(0, 1, false) X(1, 2, false) X(2, 1, true) X(3, 2, true)
 #define NFB_INST(i, t, tr) template __global__ void decode_kernel<8, t, tr>(const Params);
 NFB_VARIANTS(NFB_INST)
