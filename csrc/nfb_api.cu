@@ -311,6 +311,7 @@ struct nfb_ctx {
   cudaStream_t bstream2 = nullptr;
   cudaEvent_t bev[2] = {nullptr, nullptr};
   int bfork = 1;
+  int bskip = 0;  // measurement only (NFB_BATCH_SKIP, results garbage): 1 MLP branch, 2 attention, 4 GEMMs
   // stream-K partials per GEMM role [qkv, out, up, down, lm] (the consumer
   // kernels sum the pieces) and the plans of the current batch
   float* uws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -1545,7 +1546,7 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     uint16_t* const* bw = &c->bw[(size_t)4 * l];
     CK(launch_pdl(ln_hilo_kernel, dim3(B), dim3(256), 0, st, c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g,
                   w.ln2b, a1, a2, np));
-    TRY(ugemm(c, st, 0, bw[0], a1));
+    if (!(c->bskip & 4)) TRY(ugemm(c, st, 0, bw[0], a1));
     // batch: sequence b has its own cache; prefill: the T prompt rows share
     // the context's cache at consecutive positions (causal)
     __half* kc = reinterpret_cast<__half*>(prefill ? w.kc : c->bkc[l]);
@@ -1559,17 +1560,21 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
       CK(cudaStreamWaitEvent(c->bstream2, c->bev[0], 0));
       sm = c->bstream2;
     }
-    TRY(ugemm(c, sm, 2, bw[2], a2));
-    CK(launch_pdl(gelu_hilo_kernel, dim3(B, (mm + 255) / 256), dim3(256), 0, sm, ou, B, mm, w.bup, m.gelu_exact,
-                  ag, np));
-    TRY(ugemm(c, sm, 3, bw[3], ag));
+    if (!(c->bskip & 1)) {
+      if (!(c->bskip & 4)) TRY(ugemm(c, sm, 2, bw[2], a2));
+      CK(launch_pdl(gelu_hilo_kernel, dim3(B, (mm + 255) / 256), dim3(256), 0, sm, ou, B, mm, w.bup, m.gelu_exact,
+                    ag, np));
+      if (!(c->bskip & 4)) TRY(ugemm(c, sm, 3, bw[3], ag));
+    }
     if (c->bfork) CK(cudaEventRecord(c->bev[1], sm));
-    CK(launch_pdl(attn_prep_kernel, dim3(B, H), dim3(128), (size_t)3 * d * 4, st, oq, B, H, d, m.rotary_dims,
-                  c->bstate, c->max_seq, w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride));
-    CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(128), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
-                  c->max_seq, c->bstate, scale_log2, c->bpart, pstep, sstride));
-    CK(launch_pdl(attn_combine_kernel, dim3(B * H), dim3(128), 0, st, c->bpart, S, B, H, d, actx, np));
-    TRY(ugemm(c, st, 1, bw[1], actx));
+    if (!(c->bskip & 2)) {
+      CK(launch_pdl(attn_prep_kernel, dim3(B, H), dim3(128), (size_t)3 * d * 4, st, oq, B, H, d, m.rotary_dims,
+                    c->bstate, c->max_seq, w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride));
+      CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(128), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
+                    c->max_seq, c->bstate, scale_log2, c->bpart, pstep, sstride));
+      CK(launch_pdl(attn_combine_kernel, dim3(B * H), dim3(128), 0, st, c->bpart, S, B, H, d, actx, np));
+      if (!(c->bskip & 4)) TRY(ugemm(c, st, 1, bw[1], actx));
+    }
     if (c->bfork) CK(cudaStreamWaitEvent(st, c->bev[1], 0));
     CK(launch_pdl(residual_kernel, dim3(B, (h + 255) / 256), dim3(256), 0, st, c->bx, B, h, oz, w.bo, od, w.bd));
   }
@@ -1628,6 +1633,7 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   CK(cudaStreamCreateWithFlags(&c->bstream2, cudaStreamNonBlocking));
   for (auto& e : c->bev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (getenv("NFB_BATCH_FORK")) c->bfork = atoi(getenv("NFB_BATCH_FORK"));
+  if (getenv("NFB_BATCH_SKIP")) c->bskip = atoi(getenv("NFB_BATCH_SKIP"));
   // stream-K partials per role: tiles x pieces x n_pad x 128 (pieces depend
   // on M, K and the grid only; n_pad is largest at the largest batch)
   for (int j = 0; j < 5; ++j)
