@@ -87,7 +87,12 @@ static NcclApi& nccl_api() {
   static bool tried = false;
   if (!tried) {
     tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // NFB_NCCL_LIB (set by the Python shim to the NCCL that torch bundles):
+    // loading the system libnccl.so.2 first would make a later `import torch`
+    // bind its libnccl.so.2 dependency to that older library
+    void* h = nullptr;
+    if (const char* path = getenv("NFB_NCCL_LIB")) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (h) {
       a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");

@@ -396,15 +396,16 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return bits_f2(d);
 }
 
-// 8 fp16 weights . 8 fp32 inputs with packed FMAs (two interleaved chains).
+// 8 fp16 weights . 8 fp32 inputs with packed FMAs: one FFMA2 chain and a
+// single final add (the 8-16 rows of a consumer step supply the ILP).
 __device__ __forceinline__ float dot8x2(const uint4& w, const float2* x) {
   const __half2* hp = reinterpret_cast<const __half2*>(&w);
-  float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+  float2 a = make_float2(0.f, 0.f);
   a = ffma2(__half22float2(hp[0]), x[0], a);
-  b = ffma2(__half22float2(hp[1]), x[1], b);
+  a = ffma2(__half22float2(hp[1]), x[1], a);
   a = ffma2(__half22float2(hp[2]), x[2], a);
-  b = ffma2(__half22float2(hp[3]), x[3], b);
-  return (a.x + b.x) + (a.y + b.y);
+  a = ffma2(__half22float2(hp[3]), x[3], a);
+  return a.x + a.y;
 }
 
 // Reduce-scatter of 8 per-lane values over a warp: afterwards lane l holds the
@@ -1505,11 +1506,8 @@ struct Consumer {
             c[r] = __shfl_sync(0xffffffffu, gval, (off + r) & 31);
             c2[r] = __shfl_sync(0xffffffffu, gval, (off2 + r) & 31);
           }
-#pragma unroll
-          for (int r = 0; r < kRows; ++r) {
-            c[r] = r < dsc.n ? c[r] : 0.f;
-            c2[r] = r < dsc2.n ? c2[r] : 0.f;
-          }
+          // (rows >= n of a short stage are zero-filled by load_rows and
+          // gval is 0 on lanes without a row, so no masking is needed)
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
             if (pair) rowacc_pair(sbuf, dsc.n, sbuf2, dsc2.n, c, c2);
             else rowacc_stage(sbuf, dsc.n, c);

@@ -106,6 +106,25 @@ SIGNATURES = {
 _lib = None
 
 
+def _prefer_torch_nccl() -> None:
+    """Point the library's lazy NCCL dlopen at the NCCL torch bundles (the
+    nvidia-nccl wheel), found without importing torch: if the system
+    libnccl.so.2 were loaded first, a later `import torch` would resolve its
+    libnccl.so.2 dependency to that older library and fail."""
+    if os.environ.get("NFB_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["NFB_NCCL_LIB"] = cand
+            return
+
+
 def load():
     """Load the in-tree library; raises ImportError (no fallback) if absent."""
     global _lib
@@ -115,6 +134,7 @@ def load():
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             " (the fused decode block has no CPU fallback)")
+    _prefer_torch_nccl()
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
