@@ -61,6 +61,8 @@ struct Smem {
   float* ybuf;
   float* attst;
   float* ctx;
+  float2* ctx2;   // ctx as (c, c) pairs: the W_out^T coefficients, ready FFMA2 operands
+  float2* gpair;  // [warp][32] gelu(up) of the current batch as (g, g) pairs (W_down^T coefficients)
   float* wred;
   float* red_in;
   float* fold;
@@ -83,6 +85,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const Layout& L, cons
   s.ybuf = reinterpret_cast<float*>(base + L.ybuf);
   s.attst = reinterpret_cast<float*>(base + L.attst);
   s.ctx = reinterpret_cast<float*>(base + L.ctx);
+  s.ctx2 = reinterpret_cast<float2*>(base + L.ctx2);
+  s.gpair = reinterpret_cast<float2*>(base + L.gpair);
   s.wred = reinterpret_cast<float*>(base + L.wred);
   s.red_in = reinterpret_cast<float*>(base + L.red_in);
   s.fold = reinterpret_cast<float*>(base + L.fold);
@@ -718,8 +722,8 @@ struct Consumer {
     if (!(lane & 1) && (row < kRows ? row < n0 : row - kRows < n1)) wbase[out * p.ncw + warp] = t;
   }
 
-  __device__ __forceinline__ void rowacc_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float (&ca)[kRows],
-                                              const float (&cb)[kRows]) {
+  __device__ __forceinline__ void rowacc_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float2* ca,
+                                              const float2* cb) {
     rowacc_stage(sa, n0, ca);
     rowacc_stage(sb, n1, cb);
   }
@@ -736,7 +740,11 @@ struct Consumer {
 
   // acc += coef[r] * row r over the stage's rows (transposed projections);
   // coef[r] must be 0 for r >= n.
-  __device__ __forceinline__ void rowacc_stage(uint32_t sl, int n, const float (&coef)[kRows]) {
+  // coef[r] = (c_r, c_r) in shared memory (ctx2 / gpair): each pair comes
+  // straight from an LDS.64 at its use, so no register moves build the FFMA2
+  // operand and no 8-16 coefficients stay live across the loads.  Rows >= n
+  // of a short stage multiply zero-filled weights (coefficients finite).
+  __device__ __forceinline__ void rowacc_stage(uint32_t sl, int n, const float2* coef) {
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
       uint4 w[kRows];
@@ -744,9 +752,9 @@ struct Consumer {
 #pragma unroll
       for (int r = 0; r < kRows; ++r) {
         const __half2* hp = reinterpret_cast<const __half2*>(&w[r]);
-        const float2 c2 = make_float2(coef[r], coef[r]);
+        const float2 cr = coef[r];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc2[k][i] = ffma2(c2, __half22float2(hp[i]), acc2[k][i]);
+        for (int i = 0; i < 4; ++i) acc2[k][i] = ffma2(cr, __half22float2(hp[i]), acc2[k][i]);
       }
     }
   }
@@ -984,6 +992,8 @@ struct Consumer {
         }
       }
       s.ctx[t] = val / Lc;
+      s.ctx2[t] = make_float2(val / Lc, val / Lc);
+      if (t < 8) s.ctx2[d + t] = make_float2(0.f, 0.f);  // read (x zero weights) by short W_out stages
     }
     consumer_sync(nct);
     tock(12, t0);
@@ -1466,12 +1476,10 @@ struct Consumer {
           }
         } else if (dsc.type == ST_WO) {
           attention_complete();
-          float c[kRows], c2[kRows];
-#pragma unroll
-          for (int r = 0; r < kRows; ++r) {
-            c[r] = r < dsc.n ? s.ctx[dsc.a + r] : 0.f;
-            c2[r] = r < dsc2.n ? s.ctx[dsc2.a + r] : 0.f;
-          }
+          // rows >= n of a short stage read a context value or one of the
+          // 8 zero pairs after ctx2[d - 1] (finite x zero-filled weights)
+          const float2* c = s.ctx2 + dsc.a;
+          const float2* c2 = s.ctx2 + dsc2.a;
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
             if (NCH == 1 && pair) rowacc_pair(sbuf, dsc.n, sbuf2, dsc2.n, c, c2);
             else rowacc_stage(sbuf, dsc.n, c);
@@ -1496,16 +1504,15 @@ struct Consumer {
             const int bi = grow - ub0;
             const float gb = (bi >= 0 && bi < ubn) ? s.ubias[bi] : __ldg(W.bup + grow);
             gval = lane < pend ? gelu_f(row_total(wr) + gb, p.gelu_exact) : 0.f;
+            s.gpair[warp * 32 + lane] = make_float2(gval, gval);  // this warp's copy: a __syncwarp suffices
+            __syncwarp();
             gbuf ^= 1;
           }
         } else if (dsc.type == ST_DOWN) {
           const int off = dsc.flags >> 8, off2 = dsc2.flags >> 8;
-          float c[kRows], c2[kRows];
-#pragma unroll
-          for (int r = 0; r < kRows; ++r) {
-            c[r] = __shfl_sync(0xffffffffu, gval, (off + r) & 31);
-            c2[r] = __shfl_sync(0xffffffffu, gval, (off2 + r) & 31);
-          }
+          // (off + r <= 31: a batch holds at most 2 x 8 rows)
+          const float2* c = s.gpair + warp * 32 + off;
+          const float2* c2 = s.gpair + warp * 32 + off2;
           // (rows >= n of a short stage are zero-filled by load_rows and
           // gval is 0 on lanes without a row, so no masking is needed)
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {

@@ -136,7 +136,7 @@ constexpr int kMiscCum = 56;
 
 // Shared-memory carve-up, computed identically on host and device.
 struct Layout {
-  int ring, full, empty, desc, bars, ybuf, attst, ctx, wred, red_in, fold, rope, misc, ubias, lw, total;
+  int ring, full, empty, desc, bars, ybuf, attst, ctx, ctx2, gpair, wred, red_in, fold, rope, misc, ubias, lw, total;
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -153,6 +153,8 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.ybuf = o;   o += 4 * align_up(3 * p.d, 4);
   L.attst = o;  o += 4 * p.C * p.ncw * align_up(p.d + 2, 4);  // [rank][warp] softmax states
   L.ctx = o;    o += 4 * align_up(p.d, 4);
+  L.ctx2 = o;   o += 8 * (align_up(p.d, 4) + 8); // context as (c, c) pairs for FFMA2, + 8 zero pairs
+  L.gpair = o;  o += 8 * 32 * p.ncw;           // per warp: gelu(up) of the batch as (g, g) pairs
   L.wred = o;   o += 4 * p.ncw * (align_up(p.rows_qkv, 8) > 4 * kRows ? align_up(p.rows_qkv, 8) : 4 * kRows);
   L.red_in = o; o += 4 * (p.C - 1) * p.h;
   L.fold = o;   o += 4 * 32 * p.ncw;
