@@ -501,18 +501,6 @@ __device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
   return ((unsigned long long)u << 32) | (unsigned long long)(0xffffffffu - (uint32_t)idx);
 }
 
-// Consumer-wide sum (all ncw warps participate); `scratch` holds >= ncw floats.
-__device__ __forceinline__ float consumer_sum(float v, float* scratch, int ncw, int warp, int lane) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  consumer_sync(ncw * 32);
-  if (lane == 0) scratch[warp] = v;
-  consumer_sync(ncw * 32);
-  float t = 0.f;
-  for (int w = 0; w < ncw; ++w) t += scratch[w];
-  return t;
-}
-
 // ===========================================================================
 // Consumer
 // ===========================================================================
@@ -601,7 +589,7 @@ struct Consumer {
     if (lane == 0) mbar_arrive_u32(empty_s + 8u * sl);
   }
 
-  // ---- LayerNorm: two-pass mean / population variance (nf/golden.py:34-40);
+  // ---- LayerNorm: mean / population variance (nf/golden.py:34-49); the
   // statistics once per vector (LN1 and LN2 of the parallel residual share them)
   __device__ __forceinline__ void layer_norm(const float (&x)[NCH][8], const float* g, const float* b,
                                              float2 (&out)[NCH][4]) {
@@ -609,23 +597,39 @@ struct Consumer {
     ln_stats(x, mu, rstd);
     ln_apply(x, mu, rstd, g, b, out);
   }
+  // One consumer-wide reduction of (sum, sum of squares) -- the single-pass
+  // form of the reference's fused path (nf/cluster.py:316, variance clamped
+  // at 0) -- instead of the golden two-pass form (two reductions, four
+  // consumer barriers): activations are O(1) with |mean| << std here, so the
+  // fp32 cancellation in E[x^2] - mean^2 stays ~1e-7 relative.
   __device__ __forceinline__ void ln_stats(const float (&x)[NCH][8], float& mu_out, float& rstd_out) {
-    float sm = 0.f;
+    float sm = 0.f, sq = 0.f;
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
       if (act[k])
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sm += x[k][i];
-    const float mu = consumer_sum(sm, reinterpret_cast<float*>(s.misc) + 16, p.ncw, warp, lane) / p.h;
-    float sq = 0.f;
+        for (int i = 0; i < 8; ++i) {
+          sm += x[k][i];
+          sq = fmaf(x[k][i], x[k][i], sq);
+        }
 #pragma unroll
-    for (int k = 0; k < NCH; ++k)
-      if (act[k])
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sq += (x[k][i] - mu) * (x[k][i] - mu);
-    const float var = consumer_sum(sq, reinterpret_cast<float*>(s.misc) + 32, p.ncw, warp, lane) / p.h;
+    for (int o = 16; o > 0; o >>= 1) {
+      sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    }
+    float2* scr = reinterpret_cast<float2*>(s.misc + 16);  // misc[16..47]: ncw float2
+    consumer_sync(nct);
+    if (lane == 0) scr[warp] = make_float2(sm, sq);
+    consumer_sync(nct);
+    float ts = 0.f, tq = 0.f;
+    for (int w = 0; w < p.ncw; ++w) {
+      const float2 v = scr[w];
+      ts += v.x;
+      tq += v.y;
+    }
+    const float mu = ts / p.h;
     mu_out = mu;
-    rstd_out = rsqrtf(var + p.eps);
+    rstd_out = rsqrtf(fmaxf(tq / p.h - mu * mu, 0.f) + p.eps);
   }
   __device__ __forceinline__ void ln_apply(const float (&x)[NCH][8], float mu, float rstd, const float* g,
                                            const float* b, float2 (&out)[NCH][4]) {

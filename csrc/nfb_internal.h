@@ -159,6 +159,7 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.red_in = o; o += 4 * (p.C - 1) * p.h;
   L.fold = o;   o += 4 * 32 * p.ncw;
   L.rope = o;   o += 4 * align_up(p.rd, 4);
+  o = align_up(o, 16);
   L.misc = o;   o += 4 * 64;
   L.ubias = o;  o += 4 * kMaxBias;
   L.lw = o;     o += 2 * (int)sizeof(LayerW);
