@@ -68,7 +68,7 @@ def parse():
     if a.batch > 1:
         name = {"pythia-2.8b": "Pythia-2.8B", "pythia-6.9b": "Pythia-6.9B"}.get(a.model, a.model)
         WORKLOAD = (f"{name} random-init, batch {a.batch}, ctx {CONTEXT}, greedy decode, CUDA graph "
-                    "(cuBLAS hi/lo GEMMs + fused attention / LN / GELU kernels)")
+                    "(tcgen05 hi/lo GEMMs + TMA-tiled attention / LN / GELU kernels)")
     return a
 
 
@@ -324,7 +324,7 @@ def run_batch(args, world, rank, local):
                      "note": "bytes per step (weights once + B x KV); the step is a graph of many launches"},
         "e2e": {"value": world * B * K / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 4 * B},
-        "gpu_launches": K * (cfg.n_layers * 11 + 5),
+        "gpu_launches": K * (cfg.n_layers * 10 + 5),  # per layer: LN, 4 GEMMs, prep, tiles, combine, GELU, residual
         "clocks": clk.summary(),
         "tokens_tail": [int(x) for x in last[:5]],
     }
