@@ -343,6 +343,7 @@ struct nfb_ctx {
   int mlp_gap = 1;   // MLP pairs interleaved into the head schedule (split-phase cluster syncs)
   int fold_all = 1;  // see Params::fold_all
   int deterministic = 0;  // 1: fixed-order fold layer end (bitwise reproducible) instead of fp32 atomics
+  int acc_prereduce = 1;  // atomic layer end: DSMEM cluster pre-reduce first (NFB_ACC_PREREDUCE=0: off)
   float* acc = nullptr;   // [n_layers][hidden] atomic layer-end accumulators
   int pair = 7;      // consumer stage pairing mask (1 MLP, 2 QKV, 4 W_out)
   unsigned long long* h_tok = nullptr;  // pinned [2]
@@ -440,6 +441,7 @@ Params base_params(nfb_ctx* c) {
   p.fold_all = c->fold_all;
   p.acc = c->acc;
   p.acc_mode = (m.parallel_residual && c->tp_size == 1 && !c->deterministic) ? 1 : 0;
+  p.acc_prereduce = c->acc_prereduce;
   p.tp_root = c->tp_rank == 0 ? 1 : 0;
   p.state_update = 1;
   p.vocab_offset = c->tp_rank * c->desc.vocab;
@@ -696,6 +698,7 @@ static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, in
   if (getenv("NFB_PAIR")) c->pair = atoi(getenv("NFB_PAIR"));
   if (getenv("NFB_FOLD_ALL")) c->fold_all = atoi(getenv("NFB_FOLD_ALL")) ? 1 : 0;
   if (getenv("NFB_DETERMINISTIC")) c->deterministic = atoi(getenv("NFB_DETERMINISTIC")) ? 1 : 0;
+  if (getenv("NFB_ACC_PREREDUCE")) c->acc_prereduce = atoi(getenv("NFB_ACC_PREREDUCE")) ? 1 : 0;
   if (getenv("NFB_ASSIST")) c->assist = atoi(getenv("NFB_ASSIST"));
   if (getenv("NFB_DYN_MLP")) c->dyn_mlp = atoi(getenv("NFB_DYN_MLP")) ? 1 : 0;
   // assist needs CTAs without heads, parts of a multiple of 4 rows, <= 8 parts

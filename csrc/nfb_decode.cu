@@ -1278,9 +1278,45 @@ struct Consumer {
         }
     }
     float* dst = p.acc + (size_t)lrel * h;
+    bool contribute = true;
+    if (p.acc_prereduce && p.C > 1) {
+      // cluster pre-reduce through DSMEM: ranks 1.. bulk-copy their partial
+      // into rank 0's red_in slot (complete_tx on rank 0's bar_red); rank 0
+      // adds them in rank order and alone issues the global reductions
+      if (rank != 0) {
+        float* stg = s.red_in + (size_t)(rank - 1) * h;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          if (act[k]) {
+            float4* q = reinterpret_cast<float4*>(stg + col[k] * 8);
+            q[0] = make_float4(acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y);
+            q[1] = make_float4(acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y);
+          }
+        fence_proxy_async_smem();
+        consumer_sync(nct);
+        if (tid == 0) {
+          const uint32_t src = smem_u32(stg);
+          bulk_s2cluster(mapa(src, 0), src, (uint32_t)h * 4u, mapa(smem_u32(s.bar_red), 0));
+        }
+        contribute = false;
+      } else {
+        if (tid == 0) mbar_arrive_expect_tx_u32(smem_u32(s.bar_red), (uint32_t)((p.C - 1) * h * 4));
+        mbar_wait_u32(smem_u32(s.bar_red), n_red & 1, p.err, 13);
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          if (act[k])
+            for (int r = 1; r < p.C; ++r) {
+              const float4* q = reinterpret_cast<const float4*>(s.red_in + (size_t)(r - 1) * h + col[k] * 8);
+              const float4 a = q[0], b = q[1];
+              acc2[k][0].x += a.x; acc2[k][0].y += a.y; acc2[k][1].x += a.z; acc2[k][1].y += a.w;
+              acc2[k][2].x += b.x; acc2[k][2].y += b.y; acc2[k][3].x += b.z; acc2[k][3].y += b.w;
+            }
+      }
+      ++n_red;
+    }
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
-      if (act[k]) {
+      if (act[k] && contribute) {
         red_add_v4(dst + col[k] * 8, acc2[k][0].x, acc2[k][0].y, acc2[k][1].x, acc2[k][1].y);
         red_add_v4(dst + col[k] * 8 + 4, acc2[k][2].x, acc2[k][2].y, acc2[k][3].x, acc2[k][3].y);
       }

@@ -93,6 +93,7 @@ struct Params {
   float* part;          // [n_clusters][h] cluster partial sums
   float* acc;           // [layers][h] atomic split-K accumulators (acc_mode), all zero between launches
   int acc_mode;         // 1: layer end = red.add.v4.f32 of every CTA's partial + ONE grid barrier
+  int acc_prereduce;    // acc_mode: cluster ranks first reduce to rank 0 through DSMEM (half the atomics)
   int* ctr;             // [2][ctr_stride] dynamic chunk counters by step parity
   int ctr_stride;
   unsigned long long* gbar;  // grid barrier arrival counter (monotonic)
