@@ -374,7 +374,14 @@ UPlan umma_plan(int M, int N, int K, int sm_count) {
   P.su = 1;
   if (const char* e = getenv("NFB_UMMA_SU")) P.su = atoi(e) < 1 ? 1 : (atoi(e) > 4 ? 4 : atoi(e));
   const size_t stage = (size_t)P.su * ((size_t)kUmmaBlk + (size_t)P.n_pad * kUmmaKB * 2);
-  int s = (int)((212u * 1024u) / stage);
+  // Ring budget 80 KB, not the ~212 KB one CTA per SM could take: then the
+  // attention tile blocks (47 KB) and the small kernels of the other branch
+  // co-reside with the GEMM's CTAs, and the two branches of a layer really
+  // overlap (C4 at ctx 4096, B = 4 / 16: 1298 -> 1571 / 2774 -> 3018 tok/s;
+  // 64-96 KB equal, 40-48 KB and 128+ KB slower).  NFB_UMMA_SMEM_KB overrides.
+  size_t budget = 80u * 1024u;
+  if (const char* e = getenv("NFB_UMMA_SMEM_KB")) budget = (size_t)atoi(e) * 1024u;
+  int s = (int)(budget / stage);
   if (s > 16) s = 16;
   if (s < 2) s = 2;
   P.stages = s;
