@@ -32,6 +32,7 @@ __global__ void attn_tile_kernel(const float* q, const __half* kc, const __half*
                                  int max_seq, const int* state, float scale_log2, float* part, int pos_step,
                                  size_t seq_stride);
 size_t attn_tile_smem(int d);
+int attn_tile_positions();
 // tcgen05 GEMM (csrc/nfb_umma.cu)
 UPlan umma_plan(int M, int N, int K, int sm_count);
 size_t umma_blocked_elems(int M, int K);
@@ -1611,7 +1612,7 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   // KV tiles of 128 positions per (sequence, head) over the whole cache
   // (positions come from device state, so the grid covers max_seq; tiles
   // past the current length exit at once)
-  c->bsplit = (c->max_seq + 127) / 128;
+  c->bsplit = (c->max_seq + attn_tile_positions() - 1) / attn_tile_positions();
   if (c->bsplit > 256) return fail(NFB_EUNSUPPORTED, "batched decode needs max_seq <= 32768");
   {
     const cudaError_t e = cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

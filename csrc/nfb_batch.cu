@@ -169,7 +169,12 @@ __global__ void attn_prep_kernel(const UOut y, int B, int H, int d, int rd, cons
 // resident block has its whole tile outstanding.  Scores, max, exp2 weights
 // and P.V from shared memory; writes the tile's (m, l, o[d]) to part.  Tiles
 // at or past P (the grid covers max_seq) write an empty state.
-constexpr int kTile = 128;
+#ifndef NFB_ATTN_TILE
+#define NFB_ATTN_TILE 128
+#endif
+constexpr int kTile = NFB_ATTN_TILE;  // KV positions per attention block (128 measured best; 64: -4..-8 %)
+static_assert(kTile == 128, "attn_tile_kernel scores one position per thread of its 128-thread block");
+int attn_tile_positions() { return kTile; }
 __global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __half* kc, const __half* vc, int B,
                                                         int H, int d, int max_seq, const int* state,
                                                         float scale_log2, float* part, int pos_step,
