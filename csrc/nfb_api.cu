@@ -333,6 +333,9 @@ struct nfb_ctx {
   int* h_state = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  // serving step graphs by step parity: H2D of the input token, the decode
+  // launch, D2H of the argmax slot -- one graph launch per nfb_step_token
+  cudaGraphExec_t gtok[2] = {nullptr, nullptr};
   int decode_pos = -1;  // host mirror of the device position in decode mode
   int decode_step = 0;  // host mirror of the device step counter
   unsigned long long* trace = nullptr;
@@ -786,6 +789,8 @@ int nfb_destroy(nfb_ctx* c) {
   if (c->bgexec) cudaGraphExecDestroy(c->bgexec);
   if (c->bgraph) cudaGraphDestroy(c->bgraph);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  for (auto& g : c->gtok)
+    if (g) cudaGraphExecDestroy(g);
   if (c->graph) cudaGraphDestroy(c->graph);
   for (void* p : c->allocs) cudaFree(p);
   if (c->h_x) cudaFreeHost(c->h_x);
@@ -1238,6 +1243,11 @@ int nfb_graph_capture(nfb_ctx* c) {
     cudaGraphExecDestroy(c->gexec);
     c->gexec = nullptr;
   }
+  for (auto& gt : c->gtok)
+    if (gt) {
+      cudaGraphExecDestroy(gt);
+      gt = nullptr;
+    }
   if (c->graph) {
     cudaGraphDestroy(c->graph);
     c->graph = nullptr;
@@ -1280,6 +1290,22 @@ int nfb_graph_capture(nfb_ctx* c) {
   if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("end capture: ") + cudaGetErrorString(e2));
   c->graph = g;
   CK(cudaGraphInstantiate(&c->gexec, g, 0));
+  // the serving-step graphs (nfb_step_token): token in -> decode -> token out
+  for (int par = 0; par < 2; ++par) {
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaMemcpyAsync(c->amax + (par ^ 1), c->h_tok, 8, cudaMemcpyHostToDevice, c->stream);
+    e = launch_decode(p, variant, c->grid, c->block, c->smem, c->stream, c->coop);
+    cudaMemcpyAsync(c->h_tok + 1, c->amax + par, 8, cudaMemcpyDeviceToHost, c->stream);
+    cudaGraph_t gt = nullptr;
+    e2 = cudaStreamEndCapture(c->stream, &gt);
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+      if (gt) cudaGraphDestroy(gt);
+      return fail(NFB_ECUDA, std::string("step graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&c->gtok[par], gt, 0);
+    cudaGraphDestroy(gt);
+    if (ei != cudaSuccess) return fail(NFB_ECUDA, std::string("step graph instantiate: ") + cudaGetErrorString(ei));
+  }
   return NFB_OK;
 }
 
@@ -1305,15 +1331,19 @@ int nfb_step_token(nfb_ctx* c, int token, int* next_token) {
   const int par = c->decode_step & 1;
   // the step reads its input token from slot par^1 and writes its argmax to slot par
   c->h_tok[0] = (0xffffffffull << 32) | (unsigned long long)(0xffffffffu - (uint32_t)token);
-  CK(cudaMemcpyAsync(c->amax + (par ^ 1), c->h_tok, 8, cudaMemcpyHostToDevice, c->stream));
-  if (c->gexec) {
-    CK(cudaGraphLaunch(c->gexec, c->stream));
-  } else if (c->nccl) {
-    TRY(tp_token(c, c->stream));
+  if (c->gtok[par]) {
+    CK(cudaGraphLaunch(c->gtok[par], c->stream));  // H2D + decode + D2H in one launch
   } else {
-    TRY(launch(c, decode_params(c), c->stream));
+    CK(cudaMemcpyAsync(c->amax + (par ^ 1), c->h_tok, 8, cudaMemcpyHostToDevice, c->stream));
+    if (c->gexec) {
+      CK(cudaGraphLaunch(c->gexec, c->stream));
+    } else if (c->nccl) {
+      TRY(tp_token(c, c->stream));
+    } else {
+      TRY(launch(c, decode_params(c), c->stream));
+    }
+    CK(cudaMemcpyAsync(c->h_tok + 1, c->amax + par, 8, cudaMemcpyDeviceToHost, c->stream));
   }
-  CK(cudaMemcpyAsync(c->h_tok + 1, c->amax + par, 8, cudaMemcpyDeviceToHost, c->stream));
   TRY(check_device_error(c));
   c->decode_pos += 1;
   c->decode_step += 1;
@@ -1354,6 +1384,11 @@ int nfb_set_option(nfb_ctx* c, int option, int value) {
     cudaGraphExecDestroy(c->gexec);
     c->gexec = nullptr;
   }
+  for (auto& gt : c->gtok)
+    if (gt) {
+      cudaGraphExecDestroy(gt);
+      gt = nullptr;
+    }
   return NFB_OK;
 }
 
