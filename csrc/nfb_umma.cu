@@ -515,3 +515,20 @@ extern "C" int nfb_gemm_trace_dev(void* buf) {
   g_trace = static_cast<unsigned long long*>(buf);
   return 0;
 }
+
+// Host-only view of the GEMM plan (no device work): out[0..7] = grid, k-blocks
+// per tile, tiles, max pieces per tile, ring stages, units per stage, n_pad,
+// dynamic smem bytes.  For host-logic tests of the stream-K partition.
+extern "C" int nfb_gemm_plan(int M, int N, int K, int sm_count, int* out) {
+  if (M < 1 || N < 1 || N > 256 || K < 1 || sm_count < 1 || !out) return -1;
+  const nfb::UPlan P = nfb::umma_plan(M, N, K, sm_count);
+  out[0] = P.G;
+  out[1] = P.kb;
+  out[2] = P.tiles;
+  out[3] = P.max_pieces;
+  out[4] = P.stages;
+  out[5] = P.su;
+  out[6] = P.n_pad;
+  out[7] = (int)P.smem;
+  return 0;
+}

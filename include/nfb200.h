@@ -231,6 +231,10 @@ int nfb_gemm_f16_blocked_dev(int M, int N, int K, const void* Wb, const void* A,
 /* Diagnostics: per-CTA globaltimer stamps ([grid][8] u64, caller-owned device
  * buffer; NULL turns it off) of the following standalone GEMM launches. */
 int nfb_gemm_trace_dev(void* buf);
+/* Host-only: the GEMM's stream-K plan for an M x K weight and N activation
+ * rows on `sm_count` SMs -> out[8] = {grid, k-blocks per tile, tiles, max
+ * pieces per tile, ring stages, units per stage, n_pad, smem bytes}. */
+int nfb_gemm_plan(int M, int N, int K, int sm_count, int* out);
 
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);

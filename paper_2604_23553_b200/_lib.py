@@ -73,6 +73,7 @@ SIGNATURES = {
     "nfb_gemm_block_weights_dev": (_I, [_I, _I, _P, _P, _P]),
     "nfb_gemm_f16_blocked_dev": (_I, [_I, _I, _I, _P, _P, _P, _P]),
     "nfb_gemm_trace_dev": (_I, [_P]),
+    "nfb_gemm_plan": (_I, [_I, _I, _I, _I, _IP]),
     "nfb_forward_dev": (_I, [_P, _I, _P, _P, _P, _I, _P]),
     "nfb_begin_decode": (_I, [_P, _I, _I]),
     "nfb_decode_step": (_I, [_P, _P]),

@@ -145,3 +145,42 @@ def test_kv_cache_duck_type():
     c.append(k + 1, -k - 1)
     assert len(c) == 2
     assert np.array_equal(c.head(1)[0][1], k[1] + 1)
+
+
+def _owner(g, G, T):
+    """CTA owning stream-K unit g (csrc/nfb_umma.cuh u_owner)."""
+    return ((g + 1) * G + T - 1) // T - 1
+
+
+@pytest.mark.parametrize("M,N,K", [(7680, 8, 2560), (2560, 32, 2560), (10240, 128, 2560), (2560, 128, 10240),
+                                   (50304, 8, 2560), (300, 17, 72), (128, 256, 64)])
+def test_gemm_stream_k_plan(M, N, K):
+    """The batched GEMM's host plan (csrc/nfb_umma.cu umma_plan) against a
+    restatement: CTA i owns units [i*T/G, (i+1)*T/G) of the tiles x k-blocks
+    units, every unit has exactly one owner, a tile's pieces are the owners
+    of its units in order (the consumers sum piece slots 0..n-1, uout), and
+    no tile has more pieces than the partial-slot count the plan allocates."""
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libnfb200.so not built")
+    lib = _lib.load()
+    out = (ctypes.c_int * 8)()
+    assert lib.nfb_gemm_plan(M, N, K, 148, out) == 0
+    G, kb, tiles, max_pieces, stages, su, n_pad, smem = list(out)
+    T = tiles * kb
+    assert kb == -(-K // 64) and tiles == -(-M // 128) and n_pad == -(-N // 8) * 8
+    assert G == min(T, 148) and stages >= 2 and su >= 1 and smem <= 227 * 1024
+    starts = [i * T // G for i in range(G + 1)]
+    owner = [None] * T
+    for i in range(G):
+        for g in range(starts[i], starts[i + 1]):
+            assert owner[g] is None
+            owner[g] = i
+    assert all(o is not None for o in owner)
+    assert all(_owner(g, G, T) == owner[g] for g in range(T))
+    worst = 0
+    for t in range(tiles):
+        pieces = sorted({owner[g] for g in range(t * kb, (t + 1) * kb)})
+        assert pieces == list(range(pieces[0], pieces[-1] + 1))  # contiguous owners
+        worst = max(worst, len(pieces))
+    assert worst == max_pieces
+    assert lib.nfb_gemm_plan(M, 0, K, 148, out) < 0
