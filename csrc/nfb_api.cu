@@ -409,7 +409,7 @@ Params base_params(nfb_ctx* c) {
   p.n_clusters = c->n_clusters;
   p.ncw = c->ncw;
   p.rows_qkv = 3 * m.d_head / (c->C + c->assist);
-  p.rows_o = m.d_head / c->C;
+  p.rows_o = m.d_head / c->C;  // (average; rank r applies rows [r d / C, (r + 1) d / C))
   p.stage_rows = c->stage_rows;
   p.n_slots = c->n_slots;
   p.slot_bytes = c->slot_bytes;
@@ -632,10 +632,15 @@ static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, in
     return fail(NFB_EUNSUPPORTED, "hidden must be a multiple of 8 and <= 4096");
   if (m.d_head % 8) return fail(NFB_EUNSUPPORTED, "d_head must be a multiple of 8");
   if (max_seq < 1) return fail(NFB_EINVAL, "max_seq must be >= 1");
+  // Default cluster size: 2 CTAs per head; 3 for long contexts (max_seq >
+  // 3072), where each head's KV history is the longer part of its chain:
+  // Pythia-2.8B at ctx 4096 / 8192: 782 / 653 vs 709 / 535 tok/s, equal at
+  // 3072, worse at <= 2048 (884 vs 952 at 1024).
   int C = cluster_size > 0 ? cluster_size : 2;
+  if (cluster_size <= 0 && max_seq > 3072 && (3 * m.d_head) % 3 == 0 && (m.d_head % 4) == 0) C = 3;
   if (cluster_size <= 0 && getenv("NFB_CLUSTER")) C = atoi(getenv("NFB_CLUSTER"));
-  if (C > 8 || (3 * m.d_head) % C || m.d_head % C || ((3 * m.d_head) / C) % 4)
-    return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8, divide d_head and leave a multiple of 4 QKV rows per rank");
+  if (C > 8 || (3 * m.d_head) % C || ((3 * m.d_head) / C) % 4)
+    return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8 and leave an equal multiple of 4 QKV rows per rank");
 
   nfb_ctx* c = new nfb_ctx();
   c->desc = m;

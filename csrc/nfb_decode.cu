@@ -127,7 +127,8 @@ __device__ __forceinline__ long long head_stage_bytes(const Params& p, int k, in
   if (k >= p.H) return a;
   const int nh = (p.H - k + p.n_clusters - 1) / p.n_clusters;
   const int cnt = pos / p.C + (r < pos % p.C ? 1 : 0);
-  const long long b = (long long)nh * ((long long)(p.rows_qkv + p.rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
+  const int rows_o = (r + 1) * p.d / p.C - r * p.d / p.C;  // W_out^T rows of rank r (d need not divide by C)
+  const long long b = (long long)nh * ((long long)(p.rows_qkv + rows_o) * p.h * 2 + (long long)cnt * p.d * 4);
   return a + b * p.head_weight_pct / 100;
 }
 
@@ -339,10 +340,11 @@ struct Producer {
         }
         if (gap) emit_mlp(W, ctr, next, gap);
         // W_out^T rows (context elements) owned by this rank.
-        const int o0 = (int)rank * p.rows_o;
-        for (int r = 0, k = 0; r < p.rows_o; r += p.stage_rows, ++k) {
-          const int n = min(p.stage_rows, p.rows_o - r);
-          const int last = (r + n >= p.rows_o) ? F_LAST : 0;
+        // context rows [rank d / C, (rank + 1) d / C) (d need not divide by C)
+        const int o0 = (int)rank * d / C, rows_o = ((int)rank + 1) * d / C - o0;
+        for (int r = 0, k = 0; r < rows_o; r += p.stage_rows, ++k) {
+          const int n = min(p.stage_rows, rows_o - r);
+          const int last = (r + n >= rows_o) ? F_LAST : 0;
           const int pair = ((p.pair & 4) && !(k & 1) && !last) ? F_PAIR : 0;
           push(ST_WO, o0 + r, n, tag | last | pair, W.woT + (size_t)(hh * d + o0 + r) * h, n * rowb);
         }
