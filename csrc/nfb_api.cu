@@ -632,12 +632,13 @@ static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, in
     return fail(NFB_EUNSUPPORTED, "hidden must be a multiple of 8 and <= 4096");
   if (m.d_head % 8) return fail(NFB_EUNSUPPORTED, "d_head must be a multiple of 8");
   if (max_seq < 1) return fail(NFB_EINVAL, "max_seq must be >= 1");
-  // Default cluster size: 2 CTAs per head; 3 for long contexts (max_seq >
-  // 3072), where each head's KV history is the longer part of its chain:
-  // Pythia-2.8B at ctx 4096 / 8192: 782 / 653 vs 709 / 535 tok/s, equal at
-  // 3072, worse at <= 2048 (884 vs 952 at 1024).
+  // Default cluster size: 2 CTAs per head; 3 once a head's KV history
+  // (4 d bytes per position) outweighs ~40 % of its serial chain (QKV +
+  // W_out rows, 8 d h bytes): max_seq > 4 h / 3.  Measured, C = 2 vs 3:
+  // Pythia-2.8B ctx 1024 952 vs 884, 3072 799 vs 804, 4096 709 vs 782, 8192
+  // 535 vs 653 tok/s; Pythia-6.9B ctx 4096 345 vs 325 (threshold 5461).
   int C = cluster_size > 0 ? cluster_size : 2;
-  if (cluster_size <= 0 && max_seq > 3072 && (3 * m.d_head) % 3 == 0 && (m.d_head % 4) == 0) C = 3;
+  if (cluster_size <= 0 && 3LL * max_seq > 4LL * m.hidden && (m.d_head % 4) == 0) C = 3;
   if (cluster_size <= 0 && getenv("NFB_CLUSTER")) C = atoi(getenv("NFB_CLUSTER"));
   if (C > 8 || (3 * m.d_head) % C || ((3 * m.d_head) / C) % 4)
     return fail(NFB_EUNSUPPORTED, "cluster_size must be <= 8 and leave an equal multiple of 4 QKV rows per rank");

@@ -76,7 +76,7 @@ int nfb_version(void);
 const char* nfb_last_error(void);
 
 /* Create a context for `desc` on `device` with KV capacity `max_seq` per layer.
- * cluster_size 0 = default (2; 3 when max_seq > 3072); max_clusters 0 = as many as fit co-resident.
+ * cluster_size 0 = default (2; 3 when max_seq > 4 hidden / 3); max_clusters 0 = as many as fit co-resident.
  * Replaces constructing ModelConfig + KVCache(n_heads, d_head) (nf/weights.py:135). */
 int nfb_create(const nfb_model_desc* desc, int device, int max_seq, int cluster_size,
                int max_clusters, nfb_ctx** out);
