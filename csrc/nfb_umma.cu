@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -361,7 +362,12 @@ UPlan umma_plan(int M, int N, int K, int sm_count) {
   P.kb = (K + kUmmaKB - 1) / kUmmaKB;
   P.tiles = (M + kUmmaM - 1) / kUmmaM;
   P.total = P.tiles * P.kb;
-  P.G = P.total < sm_count ? P.total : sm_count;
+  // 1.5 CTAs per SM: with the 80 KB ring two GEMM CTAs fit an SM, and the
+  // extra CTAs fill SMs the other branch's kernels leave (C4 ctx 4096 B = 4 /
+  // 16 / 64: +1.8 / +0.6 / +0.7 % over one per SM; 2 per SM and < 1 slower).
+  int gmax = sm_count * 3 / 2;
+  if (const char* e = getenv("NFB_UMMA_GRID")) gmax = atoi(e) > 0 ? std::min(atoi(e), sm_count * 2) : gmax;
+  P.G = P.total < gmax ? P.total : gmax;
   int mp = 1;
   for (int t = 0; t < P.tiles; ++t) {
     const int c = u_owner((long long)(t + 1) * P.kb - 1, P.G, P.total) - u_owner((long long)t * P.kb, P.G, P.total) + 1;

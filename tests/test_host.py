@@ -168,7 +168,7 @@ def test_gemm_stream_k_plan(M, N, K):
     G, kb, tiles, max_pieces, stages, su, n_pad, smem = list(out)
     T = tiles * kb
     assert kb == -(-K // 64) and tiles == -(-M // 128) and n_pad == -(-N // 8) * 8
-    assert G == min(T, 148) and stages >= 2 and su >= 1 and smem <= 227 * 1024
+    assert G == min(T, 148 * 3 // 2) and stages >= 2 and su >= 1 and smem <= 227 * 1024
     starts = [i * T // G for i in range(G + 1)]
     owner = [None] * T
     for i in range(G):
