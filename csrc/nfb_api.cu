@@ -1620,7 +1620,7 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     if (!(c->bskip & 2)) {
       CK(launch_pdl(attn_prep_kernel, dim3(B, H), dim3(128), (size_t)3 * d * 4, st, oq, B, H, d, m.rotary_dims,
                     c->bstate, c->max_seq, w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride));
-      CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(128), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
+      CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(attn_tile_positions()), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
                     c->max_seq, c->bstate, scale_log2, c->bpart, pstep, sstride));
       CK(launch_pdl(attn_combine_kernel, dim3(B * H), dim3(128), 0, st, c->bpart, S, B, H, d, actx, np));
       if (!(c->bskip & 4)) TRY(ugemm(c, st, 1, bw[1], actx));

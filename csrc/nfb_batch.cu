@@ -173,9 +173,10 @@ __global__ void attn_prep_kernel(const UOut y, int B, int H, int d, int rd, cons
 #define NFB_ATTN_TILE 128
 #endif
 constexpr int kTile = NFB_ATTN_TILE;  // KV positions per attention block (128 measured best; 64: -4..-8 %)
-static_assert(kTile == 128, "attn_tile_kernel scores one position per thread of its 128-thread block");
+// (tiles of 96 / 112 / 256 positions measured: +1 % / +0 % / -7..-14 %)
+static_assert(kTile == 128, "attn_tile_kernel: one scoring thread per position of its kTile-thread block");
 int attn_tile_positions() { return kTile; }
-__global__ void __launch_bounds__(128) attn_tile_kernel(const float* q, const __half* kc, const __half* vc, int B,
+__global__ void __launch_bounds__(kTile) attn_tile_kernel(const float* q, const __half* kc, const __half* vc, int B,
                                                         int H, int d, int max_seq, const int* state,
                                                         float scale_log2, float* part, int pos_step,
                                                         size_t seq_stride) {
