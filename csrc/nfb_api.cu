@@ -457,7 +457,9 @@ Params base_params(nfb_ctx* c) {
 // The lean production kernel variant has only the default path; tracing,
 // debug modes and the experimental options run on the full variant.
 bool needs_full_variant(const nfb_ctx* c) {
-  return c->trace || c->debug || c->assist || c->pf_ahead > 0 || c->dyn_mlp || !c->fold_all;
+  // the lean variant: parallel residual with the atomic layer end only
+  const bool acc_mode = c->desc.parallel_residual && c->tp_size == 1 && !c->deterministic;
+  return c->trace || c->debug || c->assist || c->pf_ahead > 0 || c->dyn_mlp || !c->fold_all || !acc_mode;
 }
 
 int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {

@@ -294,7 +294,7 @@ struct Producer {
   __device__ __forceinline__ void run(int pos, int par, uint32_t rank, uint32_t cid) {
     const int h = p.h, d = p.d, C = p.C;
     const uint32_t rowb = (uint32_t)h * 2u;
-    const int gap = (p.parallel && !(TR && p.dyn_mlp)) ? p.mlp_gap : 0;
+    const int gap = ((!TR || p.parallel) && !(TR && p.dyn_mlp)) ? p.mlp_gap : 0;
     for (int l = p.l0; l < p.l1; ++l) {
       const LayerW& W = p.layers[l];
       const int lrel = l - p.l0;
@@ -349,7 +349,7 @@ struct Producer {
           push(ST_WO, o0 + r, n, tag | last | pair, W.woT + (size_t)(hh * d + o0 + r) * h, n * rowb);
         }
       }
-      if (!p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
+      if (TR && !p.parallel) push(ST_SYNC, 0, 0, 0, nullptr, 0);
       if (TR && pf && p.dyn_mlp) return;  // dynamic chunk grabs cannot be replayed
       emit_mlp(W, ctr, next, -1);
       push(ST_END, 0, 0, 0, nullptr, 0);
@@ -1070,7 +1070,10 @@ struct Consumer {
   // event 0: parallel END, 1: sequential SYNC (attention half), 2: sequential END
   __device__ __forceinline__ void reduce_event(int event, int lrel) {
     const int h = p.h;
-    if (p.acc_mode && event == 0) {
+    // the lean production variant is the parallel residual with the atomic
+    // layer end only; the fold (deterministic mode, tensor parallel) and the
+    // sequential residual run on the full variant (host: needs_full_variant)
+    if ((!TR || p.acc_mode) && event == 0) {
       acc_layer_end(lrel);
       return;
     }
@@ -1395,7 +1398,7 @@ struct Consumer {
         }
       } else {
         // atomic layer end: the previous layer's sum is complete in acc[lrel - 1]
-        load_vec((p.acc_mode && lrel > 0) ? p.acc + (size_t)(lrel - 1) * h : p.xs + (size_t)lrel * h, x);
+        load_vec(((!TR || p.acc_mode) && lrel > 0) ? p.acc + (size_t)(lrel - 1) * h : p.xs + (size_t)lrel * h, x);
       }
       // this CTA's up biases (static MLP range) -> smem; read at the FLUSH
       // points after a consumer barrier (the first one follows the LNs)
@@ -1408,7 +1411,7 @@ struct Consumer {
         float mu, rstd;
         ln_stats(x, mu, rstd);
         ln_apply(x, mu, rstd, W.ln1g, W.ln1b, xn1);
-        if (p.parallel) ln_apply(x, mu, rstd, W.ln2g, W.ln2b, xn2);
+        if (!TR || p.parallel) ln_apply(x, mu, rstd, W.ln2g, W.ln2b, xn2);
       }
       stamp_layer(lrel, 0);
 #pragma unroll
@@ -1563,7 +1566,7 @@ struct Consumer {
           }
           release(sl);
           if (pair) release(sl2);
-        } else if (dsc.type == ST_SYNC) {
+        } else if (TR && dsc.type == ST_SYNC) {
           release(sl);
           qkv_complete();
           attention_complete();
@@ -1576,7 +1579,7 @@ struct Consumer {
           qkv_complete();
           attention_complete();
           stamp_layer(lrel, 3);
-          reduce_event(p.parallel ? 0 : 2, lrel);
+          reduce_event((!TR || p.parallel) ? 0 : 2, lrel);
           break;
         } else {
           // unexpected stage type: poison and stop
@@ -1587,7 +1590,7 @@ struct Consumer {
     }
     if (p.head_mode != HEAD_NONE) {
       run_head();
-      if (p.acc_mode && p.l1 > p.l0) {
+      if ((!TR || p.acc_mode) && p.l1 > p.l0) {
         // every CTA read the last accumulator at the head's start (and
         // arrived then): zero this CTA's chunks of it once all have
         if (tid == 0) grid_wait(p.gbar, acc_target, p.err);
@@ -1615,7 +1618,7 @@ struct Consumer {
     stamp(4);
     const int L = p.l1 - p.l0;
     float x[NCH][8];
-    const bool from_acc = p.acc_mode && L > 0;
+    const bool from_acc = (!TR || p.acc_mode) && L > 0;
     load_vec(from_acc ? p.acc + (size_t)(L - 1) * h : p.xs + (size_t)L * h, x);
     if (from_acc) {
       consumer_sync(nct);  // all of this CTA's reads of the accumulator are done
