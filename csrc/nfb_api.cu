@@ -459,7 +459,8 @@ Params base_params(nfb_ctx* c) {
 bool needs_full_variant(const nfb_ctx* c) {
   // the lean variant: parallel residual with the atomic layer end only
   const bool acc_mode = c->desc.parallel_residual && c->tp_size == 1 && !c->deterministic;
-  return c->trace || c->debug || c->assist || c->pf_ahead > 0 || c->dyn_mlp || !c->fold_all || !acc_mode;
+  return c->trace || c->debug || c->assist || c->pf_ahead > 0 || c->dyn_mlp || !c->fold_all || !acc_mode ||
+         !c->acc_prereduce;
 }
 
 int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {

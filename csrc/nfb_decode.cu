@@ -1284,7 +1284,7 @@ struct Consumer {
     }
     float* dst = p.acc + (size_t)lrel * h;
     bool contribute = true;
-    if (p.acc_prereduce && p.C > 1) {
+    if ((!TR || p.acc_prereduce) && p.C > 1) {  // (lean variant: always)
       // cluster pre-reduce through DSMEM: ranks 1.. bulk-copy their partial
       // into rank 0's red_in slot (complete_tx on rank 0's bar_red); rank 0
       // adds them in rank order and alone issues the global reductions
