@@ -456,6 +456,18 @@ Params base_params(nfb_ctx* c) {
 
 // The lean production kernel variant has only the default path; tracing,
 // debug modes and the experimental options run on the full variant.
+bool needs_full_variant(const nfb_ctx* c);
+// Production variants compiled for the headline shapes (row strides, warp
+// counts and head size as immediates): 4 = hidden 2560 / d_head 80 (Pythia-2.8B),
+// 5 = hidden 4096 / d_head 128 (Pythia-6.9B); else the runtime-shape variant.
+int kernel_variant(const nfb_ctx* c) {
+  if (needs_full_variant(c)) return c->dpl + 2;
+  const int h = c->desc.hidden, d = c->desc.d_head;
+  if (c->dpl == 0 && h == 2560 && d == 80 && c->ncw == 10) return 4;
+  if (c->dpl == 1 && h == 4096 && d == 128 && c->ncw == 8) return 5;
+  return c->dpl;
+}
+
 bool needs_full_variant(const nfb_ctx* c) {
   // the lean variant: parallel residual with the atomic layer end only
   const bool acc_mode = c->desc.parallel_residual && c->tp_size == 1 && !c->deterministic;
@@ -464,7 +476,7 @@ bool needs_full_variant(const nfb_ctx* c) {
 }
 
 int launch(nfb_ctx* c, const Params& p, cudaStream_t st) {
-  const int variant = c->dpl + (needs_full_variant(c) ? 2 : 0);
+  const int variant = kernel_variant(c);
   cudaError_t e = launch_decode(p, variant, c->grid, c->block, c->smem, st, c->coop);
   if (e != cudaSuccess && c->coop) {
     // Cooperative + cluster launch refused: fall back to the occupancy-checked
@@ -685,9 +697,9 @@ static int create_ctx(const nfb_model_desc* desc, const nfb_model_desc* full, in
   probe.n_slots = c->n_slots;
   c->smem = make_layout(probe).total;
 
-  e = cudaFuncSetAttribute(decode_kernel_ptr(c->dpl), cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(decode_kernel_ptr(c->dpl + 2), cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem);
+  e = cudaSuccess;
+  for (int v : {c->dpl, c->dpl + 2, 4 + c->dpl})  // runtime-shape, full, and headline-shape variants
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(decode_kernel_ptr(v), cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem);
   if (e != cudaSuccess) return bail(fail(NFB_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e)));
   int nc = 0;
   e = max_active_clusters(c->dpl, C, c->block, c->smem, &nc);
@@ -1282,7 +1294,7 @@ int nfb_graph_capture(nfb_ctx* c) {
     return NFB_OK;
   }
   const Params p = decode_params(c);
-  const int variant = c->dpl + (needs_full_variant(c) ? 2 : 0);
+  const int variant = kernel_variant(c);
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   cudaError_t e = launch_decode(p, variant, c->grid, c->block, c->smem, c->stream, c->coop);
   cudaGraph_t g = nullptr;

@@ -509,8 +509,17 @@ __device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
 // NCH: 16-byte hidden chunks owned per consumer thread (chunk k of thread t is
 // t + k * nct): 1 for hidden <= 2560, 2 for wider models (hidden 4096 with 8
 // consumer warps, so every variant keeps the 384-thread register budget).
-template <int DPL, bool TR, int NCH>
+template <int DPL, bool TR, int NCH, int SH = 0>
 struct Consumer {
+  // SH: compile-time shape of the production variants (0: runtime H_() / D_();
+  // 1: hidden 2560, d_head 80 -- Pythia-2.8B; 2: hidden 4096, d_head 128 --
+  // Pythia-6.9B), so row strides, warp counts and head sizes are immediates
+  static constexpr int kHs = SH == 1 ? 2560 : SH == 2 ? 4096 : 0;
+  static constexpr int kDs = SH == 1 ? 80 : SH == 2 ? 128 : 0;
+  __device__ __forceinline__ int H_() const { return kHs ? kHs : p.h; }
+  __device__ __forceinline__ int D_() const { return kDs ? kDs : p.d; }
+  __device__ __forceinline__ int NCW_() const { return kHs ? kHs / 8 / NCH / 32 : p.ncw; }
+
   const Params& p;
   const Smem& s;
   const int tid, warp, lane, nct;
@@ -541,14 +550,14 @@ struct Consumer {
 
   __device__ __forceinline__ Consumer(const Params& p_, const Smem& s_, int tid_, uint32_t rank_, uint32_t cid_,
                       int pos_, int step_)
-      : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(p_.ncw * 32),
+      : p(p_), s(s_), tid(tid_), warp(tid_ >> 5), lane(tid_ & 31), nct(kHs ? kHs / 8 / NCH : p_.ncw * 32),
         rank(rank_), cid(cid_), pos(pos_), step(step_), par(step_ & 1),
-        rowb(p_.h * 2), ring_s(smem_u32(s_.ring)),
+        rowb(kHs ? kHs * 2 : p_.h * 2), ring_s(smem_u32(s_.ring)),
         full_s(smem_u32(s_.full)), empty_s(smem_u32(s_.empty)), desc_s(smem_u32(s_.desc)) {
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
-      const int c = tid_ + k * p_.ncw * 32;
-      act[k] = c < (p_.h >> 3);
+      const int c = tid_ + k * (kHs ? kHs / 8 / NCH : p_.ncw * 32);
+      act[k] = c < ((kHs ? kHs : p_.h) >> 3);
       col[k] = act[k] ? c : 0;
     }
   }
@@ -624,14 +633,14 @@ struct Consumer {
     if (lane == 0) scr[warp] = make_float2(sm, sq);
     consumer_sync(nct);
     float ts = 0.f, tq = 0.f;
-    for (int w = 0; w < p.ncw; ++w) {
+    for (int w = 0; w < NCW_(); ++w) {
       const float2 v = scr[w];
       ts += v.x;
       tq += v.y;
     }
-    const float mu = ts / p.h;
+    const float mu = ts / H_();
     mu_out = mu;
-    rstd_out = rsqrtf(fmaxf(tq / p.h - mu * mu, 0.f) + p.eps);
+    rstd_out = rsqrtf(fmaxf(tq / H_() - mu * mu, 0.f) + p.eps);
   }
   __device__ __forceinline__ void ln_apply(const float (&x)[NCH][8], float mu, float rstd, const float* g,
                                            const float* b, float2 (&out)[NCH][4]) {
@@ -699,7 +708,7 @@ struct Consumer {
     }
     const float t = butterfly8(v, lane);
     const int row = butterfly_row(lane);
-    if ((lane & 3) == 0 && row < n) wbase[row * p.ncw + warp] = t;
+    if ((lane & 3) == 0 && row < n) wbase[row * NCW_() + warp] = t;
   }
 
   // Two stages (rows n0 of stage A then n1 of stage B) in one pass: 16
@@ -725,7 +734,7 @@ struct Consumer {
     const float t = butterfly16(v, lane);
     const int row = butterfly16_row(lane);  // row of the pair (0..15); stage B rows start at 8
     const int out = row < kRows ? row : n0 + row - kRows;
-    if (!(lane & 1) && (row < kRows ? row < n0 : row - kRows < n1)) wbase[out * p.ncw + warp] = t;
+    if (!(lane & 1) && (row < kRows ? row < n0 : row - kRows < n1)) wbase[out * NCW_() + warp] = t;
   }
 
   __device__ __forceinline__ void rowacc_pair(uint32_t sa, int n0, uint32_t sb, int n1, const float2* ca,
@@ -737,7 +746,7 @@ struct Consumer {
   __device__ __forceinline__ float row_total(const float* wrow) const {
     float t[kMaxConsumerWarps];
 #pragma unroll
-    for (int w = 0; w < kMaxConsumerWarps; ++w) t[w] = w < p.ncw ? wrow[w] : 0.f;
+    for (int w = 0; w < kMaxConsumerWarps; ++w) t[w] = w < NCW_() ? wrow[w] : 0.f;
     float a = 0.f;
 #pragma unroll
     for (int w = 0; w < kMaxConsumerWarps; ++w) a += t[w];
@@ -766,7 +775,7 @@ struct Consumer {
   }
 
   // ---- attention -----------------------------------------------------------
-  __device__ __forceinline__ int tpp() const { return p.d / DPL; }
+  __device__ __forceinline__ int tpp() const { return D_() / DPL; }
 
   // Rotated component j of a head vector stored at `v` (RoPE pairs (i, i+rd/2),
   // nf/golden.py:68-92); table row = this step's position.
@@ -824,9 +833,9 @@ struct Consumer {
     const int T = tpp(), gpw = 32 / T;
     const int sub = lane % T, gw = lane / T;
     const bool valid = gw < gpw;
-    const int span = p.ncw * gpw * kPos;
+    const int span = NCW_() * gpw * kPos;
     const __half* K = reinterpret_cast<const __half*>(sl);
-    const __half* Vv = K + (size_t)n * p.d;
+    const __half* Vv = K + (size_t)n * D_();
     for (int b = warp * gpw * kPos; b < n; b += span) {
       const int p0 = b + gw * kPos;
       float sc[kPos];
@@ -837,8 +846,8 @@ struct Consumer {
         float part = 0.f;
 #pragma unroll
         for (int c = 0; c < DPL / 8; ++c) {
-          const uint4 kw = *reinterpret_cast<const uint4*>(K + (size_t)ps * p.d + sub * DPL + 8 * c);
-          vw[k][c] = *reinterpret_cast<const uint4*>(Vv + (size_t)ps * p.d + sub * DPL + 8 * c);
+          const uint4 kw = *reinterpret_cast<const uint4*>(K + (size_t)ps * D_() + sub * DPL + 8 * c);
+          vw[k][c] = *reinterpret_cast<const uint4*>(Vv + (size_t)ps * D_() + sub * DPL + 8 * c);
           float kf[8];
           h8_to_f32(kw, kf);
 #pragma unroll
@@ -901,8 +910,8 @@ struct Consumer {
 #pragma unroll
       for (int i = 0; i < DPL; ++i) {
         const int j = sub * DPL + i;
-        part = fmaf(qr[i], rope_at(s.ybuf + p.d, j), part);
-        vv[i] = s.ybuf[2 * p.d + j];
+        part = fmaf(qr[i], rope_at(s.ybuf + D_(), j), part);
+        vv[i] = s.ybuf[2 * D_() + j];
       }
     }
     const float sc = group_dot(part, T, sub);
@@ -933,7 +942,7 @@ struct Consumer {
   // stage, so MLP stages in between run while the partner rank catches up).
   __device__ __forceinline__ void attention_publish() {
     const int T = tpp(), gpw = 32 / T, sub = lane % T;
-    const int d = p.d;
+    const int d = D_();
     // 1) fold the warp's groups into group 0 (lanes 0..T-1)
     for (int g2 = 1; g2 < gpw; ++g2) {
       const int src = g2 * T + sub;
@@ -946,8 +955,8 @@ struct Consumer {
     }
     // 2) the warp's state -> attst[rank][warp]; the whole rank block goes to
     //    every peer in one bulk DSMEM copy (no intra-CTA merge pass)
-    const int blk = p.ncw * s.attst_stride;
-    float* ws = s.attst + ((int)rank * p.ncw + warp) * s.attst_stride;
+    const int blk = NCW_() * s.attst_stride;
+    float* ws = s.attst + ((int)rank * NCW_() + warp) * s.attst_stride;
     if (lane < T) {
 #pragma unroll
       for (int i = 0; i < DPL; ++i) ws[sub * DPL + i] = o[i];
@@ -974,14 +983,14 @@ struct Consumer {
   __device__ __forceinline__ void attention_complete() {
     if (!att_pending) return;
     att_pending = false;
-    const int d = p.d;
+    const int d = D_();
     long long t0 = tick();
     mbar_wait_u32(smem_u32(s.bar_att), n_att & 1, p.err, 12);
     tock(11, t0);
     t0 = tick();
     ++n_att;
     // 3) merge the C * ncw (rank, warp) states in that fixed order -> context
-    const int ns = p.C * p.ncw;
+    const int ns = p.C * NCW_();
     float Mc = -INFINITY;
     for (int k = 0; k < ns; ++k) {
       const float* a = s.attst + k * s.attst_stride;
@@ -1044,7 +1053,7 @@ struct Consumer {
       }
       consumer_sync(nct);
       const int r0 = p.C * p.rows_qkv;
-      for (int t = tid; t < 3 * p.d - r0; t += nct) s.ybuf[r0 + t] = __ldcg(p.yg + (size_t)head * 3 * p.d + r0 + t);
+      for (int t = tid; t < 3 * D_() - r0; t += nct) s.ybuf[r0 + t] = __ldcg(p.yg + (size_t)head * 3 * D_() + r0 + t);
       consumer_sync(nct);
     }
     tock(8, t0);
@@ -1054,10 +1063,10 @@ struct Consumer {
     // Rank 0 appends this step's rotated key and value to the cache (fp16).
     if (rank == 0) {
       const LayerW& W = s.lw[(cur_layer - p.l0) & 1];
-      const size_t off = ((size_t)head * p.max_seq + pos) * p.d;
-      for (int j = tid; j < p.d; j += nct) {
-        W.kc[off + j] = __float2half_rn(rope_at(s.ybuf + p.d, j));
-        W.vc[off + j] = __float2half_rn(s.ybuf[2 * p.d + j]);
+      const size_t off = ((size_t)head * p.max_seq + pos) * D_();
+      for (int j = tid; j < D_(); j += nct) {
+        W.kc[off + j] = __float2half_rn(rope_at(s.ybuf + D_(), j));
+        W.vc[off + j] = __float2half_rn(s.ybuf[2 * D_() + j]);
       }
     }
     attention_begin();
@@ -1069,7 +1078,7 @@ struct Consumer {
   // ---- layer-end reduction -------------------------------------------------
   // event 0: parallel END, 1: sequential SYNC (attention half), 2: sequential END
   __device__ __forceinline__ void reduce_event(int event, int lrel) {
-    const int h = p.h;
+    const int h = H_();
     // the lean production variant is the parallel residual with the atomic
     // layer end only; the fold (deterministic mode, tensor parallel) and the
     // sequential residual run on the full variant (host: needs_full_variant)
@@ -1251,7 +1260,7 @@ struct Consumer {
   // zeroed after the head, see run()).
   unsigned long long acc_target = 0;
   __device__ __forceinline__ void acc_layer_end(int lrel) {
-    const int h = p.h, G = gridDim.x;
+    const int h = H_(), G = gridDim.x;
     const LayerW& W = s.lw[lrel & 1];
     if (blockIdx.x == 0) {
       // the layer's residual input, re-read (not kept live in registers
@@ -1371,7 +1380,7 @@ struct Consumer {
 
   // ---- main loop --------------------------------------------------------------
   __device__ __forceinline__ void run() {
-    const int h = p.h;
+    const int h = H_();
     epoch_base = (unsigned)s.misc[5];
     stamp(2);
     for (int l = p.l0; l < p.l1; ++l) {
@@ -1459,11 +1468,11 @@ struct Consumer {
           kv_first = true;
           if (dsc.flags & F_FIRST) {
             pend = 0;
-            qbias = tid < p.rows_qkv ? __ldg(W.bqkv + head * 3 * p.d + (int)rank * p.rows_qkv + tid) : 0.f;
+            qbias = tid < p.rows_qkv ? __ldg(W.bqkv + head * 3 * D_() + (int)rank * p.rows_qkv + tid) : 0.f;
           }
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
-            if (NCH == 1 && pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn1, s.wred + pend * p.ncw);
-            else rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
+            if (NCH == 1 && pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn1, s.wred + pend * NCW_());
+            else rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * NCW_());
           }
           release(sl);
           if (pair) release(sl2);
@@ -1475,8 +1484,8 @@ struct Consumer {
             consumer_sync(nct);
             const int q0 = (int)rank * p.rows_qkv;
             for (int t = tid; t < p.rows_qkv; t += nct) {
-              const float b = t < nct ? qbias : __ldg(W.bqkv + head * 3 * p.d + q0 + t);
-              s.ybuf[q0 + t] = row_total(s.wred + t * p.ncw) + b;
+              const float b = t < nct ? qbias : __ldg(W.bqkv + head * 3 * D_() + q0 + t);
+              s.ybuf[q0 + t] = row_total(s.wred + t * NCW_()) + b;
             }
             fence_proxy_async_smem();
             qkv_publish(head);
@@ -1485,15 +1494,15 @@ struct Consumer {
         } else if (TR && dsc.type == ST_AQKV) {
           // assist part of head u / A: row-dots, then publish to global
           if (dsc.flags & F_FIRST) pend = 0;
-          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * p.ncw);
+          if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + pend * NCW_());
           release(sl);
           pend += dsc.n;
           if (last) {
             const int u = head, hh = u / p.assist, q0 = dsc.a + dsc.n - p.rows_qkv;
             consumer_sync(nct);
-            float* yg = p.yg + (size_t)hh * 3 * p.d + q0;
+            float* yg = p.yg + (size_t)hh * 3 * D_() + q0;
             for (int t = tid; t < p.rows_qkv; t += nct)
-              __stcg(yg + t, row_total(s.wred + t * p.ncw) + __ldg(W.bqkv + hh * 3 * p.d + q0 + t));
+              __stcg(yg + t, row_total(s.wred + t * NCW_()) + __ldg(W.bqkv + hh * 3 * D_() + q0 + t));
             consumer_sync(nct);
             if (tid == 0) {
               __threadfence();
@@ -1535,7 +1544,7 @@ struct Consumer {
           if (dsc.flags & F_FIRST) pend = 0;
           if (lane >= pend && lane < pend + dsc.n) grow = dsc.a + lane - pend;
           if (pair && lane >= pend + dsc.n && lane < pend + dsc.n + dsc2.n) grow = dsc2.a + lane - pend - dsc.n;
-          float* wb = s.wred + (gbuf * 2 * kRows + pend) * p.ncw;
+          float* wb = s.wred + (gbuf * 2 * kRows + pend) * NCW_();
           if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) {
             if (pair) rowdot_pair(sbuf, dsc.n, sbuf2, dsc2.n, xn2, wb);
             else rowdot_stage(sbuf, dsc.n, xn2, wb);
@@ -1545,7 +1554,7 @@ struct Consumer {
           pend += dsc.n + dsc2.n;
           if ((dsc.flags | dsc2.flags) & F_FLUSH) {
             consumer_sync(nct);
-            const float* wr = s.wred + (gbuf * 2 * kRows + lane) * p.ncw;
+            const float* wr = s.wred + (gbuf * 2 * kRows + lane) * NCW_();
             const int bi = grow - ub0;
             const float gb = (bi >= 0 && bi < ubn) ? s.ubias[bi] : __ldg(W.bup + grow);
             gval = lane < pend ? gelu_f(row_total(wr) + gb, p.gelu_exact) : 0.f;
@@ -1614,7 +1623,7 @@ struct Consumer {
   }
 
   __device__ __forceinline__ void run_head() {
-    const int h = p.h;
+    const int h = H_();
     stamp(4);
     const int L = p.l1 - p.l0;
     float x[NCH][8];
@@ -1646,14 +1655,14 @@ struct Consumer {
         } else {
           lm_a1 = dsc.a;
         }
-        if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * p.ncw);
+        if (!((TR ? p.debug : 0) & DBG_NO_COMPUTE)) rowdot_stage(sbuf, dsc.n, xn1, s.wred + (gbuf * 2 * kRows + pend) * NCW_());
         release(sl);
         pend += dsc.n;
         if (dsc.flags & F_FLUSH) {
           consumer_sync(nct);
           if (warp == 0 && lane < pend) {
             const int row = lane < lm_n0 ? lm_a0 + lane : lm_a1 + lane - lm_n0;
-            const float lg = row_total(s.wred + (gbuf * 2 * kRows + lane) * p.ncw);
+            const float lg = row_total(s.wred + (gbuf * 2 * kRows + lane) * NCW_());
             if (p.logits) p.logits[row] = lg;
             const unsigned long long k = pack_argmax(lg, row + p.vocab_offset);
             best = k > best ? k : best;
@@ -1681,7 +1690,7 @@ struct Consumer {
 // ===========================================================================
 // Kernel
 // ===========================================================================
-template <int DPL, int NCH, bool TR>
+template <int DPL, int NCH, bool TR, int SH>
 __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Layout L = make_layout(p);
@@ -1750,20 +1759,23 @@ __global__ void __launch_bounds__(384, 1) decode_kernel(const Params p) {
     prod.mlp_c1 = s.misc[4];
     prod.run(pos, step & 1, rank, cid);
   } else if (warp < p.ncw) {
-    Consumer<DPL, TR, NCH> c(p, s, tid, rank, cid, pos, step);
+    Consumer<DPL, TR, NCH, SH> c(p, s, tid, rank, cid, pos, step);
     c.run();
   }
   cluster_sync_all();
 }
 
 // Kernel variants: 1 or 2 hidden chunks per consumer thread (hidden <= 2560 /
-// <= 5120), each as the lean production variant or the FULL variant (TR =
-// true: trace + measurement-debug paths and the optional experimental paths
-// -- QKV assist, L2 prefetcher warp, work-stealing MLP, cluster pre-reduce
-// fold -- compiled in; variant = (NCH - 1) + 2 * full).  Blocks are always
-// <= 384 threads.
-#define NFB_VARIANTS(X) X(0, 1, false) X(1, 2, false) X(2, 1, true) X(3, 2, true)
-#define NFB_INST(i, t, tr) template __global__ void decode_kernel<8, t, tr>(const Params);
+// <= 5120), each as the lean production variant (parallel residual, atomic
+// layer end) or the FULL variant (TR = true: the fold, the sequential
+// residual, trace + measurement-debug paths and the experimental paths --
+// QKV assist, L2 prefetcher warp, work-stealing MLP -- compiled in); variant
+// = (NCH - 1) + 2 * full, plus the lean variants specialised for the headline
+// shapes (4: hidden 2560 / d_head 80, 5: hidden 4096 / d_head 128).  Blocks
+// are always <= 384 threads.
+#define NFB_VARIANTS(X) \
+  X(0, 1, false, 0) X(1, 2, false, 0) X(2, 1, true, 0) X(3, 2, true, 0) X(4, 1, false, 1) X(5, 2, false, 2)
+#define NFB_INST(i, t, tr, sh) template __global__ void decode_kernel<8, t, tr, sh>(const Params);
 NFB_VARIANTS(NFB_INST)
 
 }  // namespace nfb
@@ -1774,8 +1786,8 @@ NFB_VARIANTS(NFB_INST)
 namespace nfb {
 
 const void* decode_kernel_ptr(int variant) {
-#define NFB_PTR(i, t, tr) \
-  if (variant == i) return reinterpret_cast<const void*>(&decode_kernel<8, t, tr>);
+#define NFB_PTR(i, t, tr, sh) \
+  if (variant == i) return reinterpret_cast<const void*>(&decode_kernel<8, t, tr, sh>);
   NFB_VARIANTS(NFB_PTR)
 #undef NFB_PTR
   return nullptr;
@@ -1801,8 +1813,8 @@ cudaError_t launch_decode(const Params& p, int variant, int grid, int block, int
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-#define NFB_LAUNCH(i, t, tr) \
-  if (variant == i) return cudaLaunchKernelEx(&cfg, decode_kernel<8, t, tr>, p);
+#define NFB_LAUNCH(i, t, tr, sh) \
+  if (variant == i) return cudaLaunchKernelEx(&cfg, decode_kernel<8, t, tr, sh>, p);
   NFB_VARIANTS(NFB_LAUNCH)
 #undef NFB_LAUNCH
   return cudaErrorInvalidValue;
