@@ -50,6 +50,14 @@ __global__ void advance_kernel(int* state, unsigned long long* amax, int* tokens
 cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int smem, cudaStream_t st,
                           bool cooperative);
 cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out);
+// single-head split-KV attention / atomic output projection (csrc/nfb_split.cu)
+cudaError_t launch_attend_split(const double* q, const double* K, const double* V, int seq, int d, int n, int mode,
+                                uint64_t seed, double scale, double* logits, double* states, int* order,
+                                void* scratch, double* out, cudaStream_t st);
+size_t attend_split_scratch_bytes(int n, int d);
+cudaError_t launch_project_atomic(const double* P, const double* W, const double* bias, const double* residual,
+                                  int n, int hidden, int fp16, uint64_t seed, double* proj, int* order, double* out,
+                                  cudaStream_t st);
 }  // namespace nfb
 
 using namespace nfb;
@@ -1875,6 +1883,86 @@ int nfb_prefill(nfb_ctx* c, int pos, int count, const float* x_in, float* x_out)
   TRY(check_device_error(c));
   for (auto& b : c->layers) b.kv_len = pos + count;
   c->decode_pos = -1;
+  return NFB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Unit-level helpers of the reference's cluster simulator (csrc/nfb_split.cu):
+// host float64 arrays in and out, device scratch per call, synchronous on the
+// current device's legacy stream.
+}  // extern "C"
+
+namespace {
+struct DevScratch {
+  std::vector<void*> ptrs;
+  ~DevScratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  cudaError_t get(T** p, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, bytes ? bytes : 8);
+    if (e == cudaSuccess) ptrs.push_back(q);
+    *p = static_cast<T*>(q);
+    return e;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+int nfb_attend_split(const double* q, const double* keys, const double* values, int seq_len, int d, int n_blocks,
+                     int merge, uint64_t seed, double scale, double* out) {
+  if (!q || !keys || !values || !out) return fail(NFB_EINVAL, "null argument");
+  if (seq_len < 1) return fail(NFB_EINVAL, "attention over empty cache");
+  if (d < 1 || n_blocks < 1) return fail(NFB_EINVAL, "d and n_blocks must be >= 1");
+  if (merge < NFB_MERGE_EXACT || merge > NFB_MERGE_PERMUTED) return fail(NFB_EINVAL, "unknown merge order");
+  if (merge == NFB_MERGE_TREE && (n_blocks & (n_blocks - 1)))
+    return fail(NFB_EINVAL, "tree merge needs a power-of-two n_blocks");
+  const size_t kv = (size_t)seq_len * d * sizeof(double);
+  DevScratch s;
+  double *dq, *dk, *dv, *lg, *st, *o;
+  int* ord;
+  void* sc;
+  CK(s.get(&dq, d * sizeof(double)));
+  CK(s.get(&dk, kv));
+  CK(s.get(&dv, kv));
+  CK(s.get(&lg, seq_len * sizeof(double)));
+  CK(s.get(&st, (size_t)n_blocks * (d + 2) * sizeof(double)));
+  CK(s.get(&o, d * sizeof(double)));
+  CK(s.get(&ord, n_blocks * sizeof(int)));
+  CK(s.get(&sc, attend_split_scratch_bytes(n_blocks, d)));
+  CK(cudaMemcpy(dq, q, d * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dk, keys, kv, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dv, values, kv, cudaMemcpyHostToDevice));
+  const int mode = n_blocks == 1 ? 4 : merge;
+  CK(launch_attend_split(dq, dk, dv, seq_len, d, n_blocks, mode, seed, scale, lg, st, ord, sc, o, nullptr));
+  CK(cudaMemcpy(out, o, d * sizeof(double), cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+int nfb_output_project_atomic(const double* partials, const double* w_out, const double* b_out,
+                              const double* residual, int n_blocks, int hidden, int fp16, uint64_t seed,
+                              double* out) {
+  if (!partials || !w_out || !b_out || !residual || !out) return fail(NFB_EINVAL, "null argument");
+  if (n_blocks < 1 || hidden < 1) return fail(NFB_EINVAL, "n_blocks and hidden must be >= 1");
+  const size_t h8 = (size_t)hidden * sizeof(double);
+  DevScratch s;
+  double *dp, *dw, *db, *dr, *pr, *o;
+  int* ord;
+  CK(s.get(&dp, n_blocks * h8));
+  CK(s.get(&dw, hidden * h8));
+  CK(s.get(&db, h8));
+  CK(s.get(&dr, h8));
+  CK(s.get(&pr, n_blocks * h8));
+  CK(s.get(&ord, (size_t)hidden * n_blocks * sizeof(int)));
+  CK(s.get(&o, h8));
+  CK(cudaMemcpy(dp, partials, n_blocks * h8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, w_out, hidden * h8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(db, b_out, h8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dr, residual, h8, cudaMemcpyHostToDevice));
+  CK(launch_project_atomic(dp, dw, db, dr, n_blocks, hidden, fp16 ? 1 : 0, seed, pr, ord, o, nullptr));
+  CK(cudaMemcpy(out, o, h8, cudaMemcpyDeviceToHost));
   return NFB_OK;
 }
 }  // extern "C"

@@ -236,6 +236,33 @@ int nfb_gemm_trace_dev(void* buf);
  * pieces per tile, ring stages, units per stage, n_pad, smem bytes}. */
 int nfb_gemm_plan(int M, int N, int K, int sm_count, int* out);
 
+/* Unit-level helpers of the reference's cluster simulator, on the GPU
+ * (csrc/nfb_split.cu; float64 host arrays, synchronous, current device).
+ *
+ * nfb_attend_split replaces neoxfuse.cluster.attend_split (nf/cluster.py:211-242):
+ * one head, q[d], keys/values[seq_len][d]; the history split into n_blocks
+ * ranges by the partition_kv rule (nf/cluster.py:134-150), one softmax state
+ * per range, merged in `merge` order: NFB_MERGE_EXACT (closed form,
+ * nf/cluster.py:172-181), RING, TREE (power-of-two n_blocks; the caller
+ * resolves non-powers to RING with the reference's warning) or PERMUTED
+ * (order permutation(n_blocks, seed), nf/halfnum.py:62-74).  out[d].
+ *
+ * nfb_output_project_atomic replaces neoxfuse.cluster.output_project_atomic
+ * (nf/cluster.py:253-285): partials[n_blocks][hidden] projected through
+ * w_out[hidden][hidden] and accumulated into residual + b_out; fp16 != 0
+ * models FP16 atomic adds (per element j: order permutation(n_blocks,
+ * counter_rand_u64(seed, j)), binary16 rounding after every add), else the
+ * block contributions are summed in float64.  out[hidden]. */
+#define NFB_MERGE_EXACT 0
+#define NFB_MERGE_RING 1
+#define NFB_MERGE_TREE 2
+#define NFB_MERGE_PERMUTED 3
+int nfb_attend_split(const double* q, const double* keys, const double* values, int seq_len, int d, int n_blocks,
+                     int merge, uint64_t seed, double scale, double* out);
+int nfb_output_project_atomic(const double* partials, const double* w_out, const double* b_out,
+                              const double* residual, int n_blocks, int hidden, int fp16, uint64_t seed,
+                              double* out);
+
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
 

@@ -8,7 +8,8 @@ runs as one hand-written sm_100a kernel (``libnfb200.so``, C-ABI in
 
 from .cluster import (
     RING, TREE, ClusterSpec, ExecTrace, KernelTraceRecord, Precision, ReductionKind,
-    ReductionStrategy, build_trace, fused_block_step, invalidate_weights, partition_kv,
+    ReductionStrategy, attend_split, build_trace, fused_block_step, invalidate_weights, output_project_atomic,
+    partition_kv,
     release_device_state,
     ring_steps, trace_to_jsonl, tree_steps,
 )

@@ -16,6 +16,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "nfb200.h")
 
 NFB_OK, NFB_EINVAL, NFB_ECUDA, NFB_ESTATE, NFB_EUNSUPPORTED, NFB_EDEVICE = 0, -1, -2, -3, -4, -5
 NFB_F64, NFB_F32, NFB_F16 = 0, 1, 2
+MERGE_EXACT, MERGE_RING, MERGE_TREE, MERGE_PERMUTED = 0, 1, 2, 3
 HEAD_NONE, HEAD_PROBE, HEAD_LM = 0, 1, 2
 OPT_TRACE, OPT_DYNAMIC_MLP, OPT_PREFETCH_KB, OPT_HEAD_WEIGHT, OPT_ASSIST, OPT_DETERMINISTIC = 1, 2, 3, 4, 5, 6
 
@@ -102,6 +103,8 @@ SIGNATURES = {
     "nfb_batch_graph_capture": (_I, [_P]),
     "nfb_batch_read_tokens": (_I, [_P, _IP]),
     "nfb_prefill": (_I, [_P, _I, _I, _FP, _FP]),
+    "nfb_attend_split": (_I, [_P, _P, _P, _I, _I, _I, _I, C.c_uint64, C.c_double, _P]),
+    "nfb_output_project_atomic": (_I, [_P, _P, _P, _P, _I, _I, _I, C.c_uint64, _P]),
 }
 
 _lib = None

@@ -7,9 +7,15 @@ state merge, split-K partials) and a fixed-order cross-cluster fold.
 
 Numerics: fp16 weights and KV cache, fp32 activations / accumulation, fixed
 reduction order (deterministic run to run).  The reference's FP16-atomic
-*emulation* (``Precision.FP16``, nf/cluster.py:253-285) is not reproduced:
-the B200 kernel has no FP16 atomics anywhere, so ``accumulation_precision``
-only affects the returned trace, exactly as ``plan`` does.
+*emulation* (``Precision.FP16``, nf/cluster.py:253-285) is not part of the
+fused block: the B200 kernel has no FP16 atomics anywhere, so in
+``fused_block_step`` ``accumulation_precision`` only affects the returned
+trace, exactly as ``plan`` does.
+
+The reference's unit-level helpers ``attend_split`` and
+``output_project_atomic`` (nf/cluster.py:211-285) run on the GPU too
+(csrc/nfb_split.cu, float64 like the reference's), with every merge order
+and the seeded FP16-atomic model.
 """
 
 from __future__ import annotations
@@ -22,6 +28,7 @@ from enum import Enum
 
 import numpy as np
 
+from . import _lib
 from .engine import Engine
 from .plans import FusionPlan, Op, kernel_layer_bytes
 
@@ -140,6 +147,67 @@ def _resolve_reduction(strategy: ReductionStrategy, n: int) -> ReductionStrategy
                       RuntimeWarning, stacklevel=3)
         return ReductionStrategy(ReductionKind.RING, strategy.seed)
     return strategy
+
+
+_MERGE = {ReductionKind.RING: _lib.MERGE_RING, ReductionKind.TREE: _lib.MERGE_TREE,
+          ReductionKind.PERMUTED_ATOMIC: _lib.MERGE_PERMUTED}
+
+
+def attend_split(q, keys, values, spec: ClusterSpec, scale: float):
+    """Split-KV attention for one head on the GPU (nf/cluster.py:211-242).
+    Returns (output, ExecTrace).  The history is split into spec.n_blocks
+    partition_kv ranges, one device CTA per range computes its softmax state
+    and the states merge in closed form (EXACT) or in the reduction
+    strategy's order (ring / tree / seed-keyed permutation), in float64."""
+    keys = np.ascontiguousarray(keys, dtype=np.float64)
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1)
+    if keys.shape[0] == 0:
+        raise ValueError("attention over empty cache")
+    if keys.ndim != 2 or values.shape != keys.shape or q.shape[0] != keys.shape[1]:
+        raise ValueError("keys and values must be [seq, d] and q [d]")
+    strategy = _resolve_reduction(spec.reduction, spec.n_blocks)
+    n = spec.n_blocks
+    merge = _lib.MERGE_EXACT if spec.accumulation_precision is Precision.EXACT else _MERGE[strategy.kind]
+    out = np.empty(values.shape[1])
+    lib = _lib.load()
+    _lib.check(lib.nfb_attend_split(_lib.vptr(q), _lib.vptr(keys), _lib.vptr(values), keys.shape[0],
+                                    keys.shape[1], n, merge, strategy.seed & (2**64 - 1), float(scale),
+                                    _lib.vptr(out)), "attend_split")
+    return out, attend_trace(keys.shape[0], values.shape[-1], n, strategy)
+
+
+def attend_trace(seq_len: int, d: int, n: int, strategy: ReductionStrategy) -> ExecTrace:
+    """The one-record trace of ``attend_split`` (nf/cluster.py:230-241): fp16
+    KV history read off-chip, (n - 1) fp32 states exchanged on-chip."""
+    rec = KernelTraceRecord(name="attend", bytes_offchip=2 * seq_len * d * 2,
+                            bytes_onchip=(n - 1) * (d + 2) * _ONCHIP_ELEM,
+                            sync_steps=strategy.steps(n), dsmem_exchanges=n - 1)
+    return ExecTrace(records=[rec])
+
+
+def output_project_atomic(context_partials, w_out, b_out, residual, spec: ClusterSpec) -> np.ndarray:
+    """Project per-block context shares and accumulate them into
+    ``residual + b_out`` on the GPU (nf/cluster.py:253-285).  FP16 precision
+    models FP16 atomic adds: per output element j the blocks are added in
+    the order permutation(n_blocks, counter_rand_u64(atomic_seed, j)) with
+    binary16 rounding after every add; EXACT sums them in float64."""
+    partials = np.ascontiguousarray(context_partials, dtype=np.float64)
+    if partials.ndim != 2 or partials.shape[0] != spec.n_blocks:
+        raise ValueError("context_partials must be [n_blocks, hidden]")
+    hidden = partials.shape[1]
+    w = np.ascontiguousarray(w_out, dtype=np.float64)
+    if w.shape != (hidden, hidden):
+        raise ValueError("w_out must be [hidden, hidden]")
+    b = np.ascontiguousarray(np.broadcast_to(np.asarray(b_out, dtype=np.float64), (hidden,)))
+    r = np.ascontiguousarray(np.broadcast_to(np.asarray(residual, dtype=np.float64), (hidden,)))
+    out = np.empty(hidden)
+    fp16 = int(spec.accumulation_precision is Precision.FP16)
+    lib = _lib.load()
+    _lib.check(lib.nfb_output_project_atomic(_lib.vptr(partials), _lib.vptr(w), _lib.vptr(b), _lib.vptr(r),
+                                             spec.n_blocks, hidden, fp16, spec.atomic_seed & (2**64 - 1),
+                                             _lib.vptr(out)), "output_project_atomic")
+    return out
 
 
 def build_trace(cfg, spec: ClusterSpec, plan: FusionPlan, seq_len: int, elem_size: int,

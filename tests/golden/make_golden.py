@@ -200,7 +200,49 @@ def prefill():
     np.savez(OUT / "prefill.npz", **out)
 
 
-ALL = [cli_fixture, prng, half, synth, blocks, fidelity, bytes_model, prefill]
+def split():
+    """attend_split and output_project_atomic (nf/cluster.py:211-285): one
+    head's split-KV attention under every merge order / precision, and the
+    atomic output projection, exact and FP16-atomic, over several seeds."""
+    import warnings
+    from neoxfuse.cluster import attend_split, output_project_atomic
+    from neoxfuse.halfnum import RING, TREE, Precision, permuted_atomic
+    rng = np.random.default_rng(47)
+    out = {}
+    strategies = {"ring": RING, "tree": TREE, "perm7": permuted_atomic(7), "perm123": permuted_atomic(123)}
+    for d, seq in ((64, 1), (80, 5), (64, 37), (80, 300)):
+        tag = f"d{d}s{seq}"
+        q = rng.standard_normal(d) * 0.8
+        K = rng.standard_normal((seq, d)) * 0.8
+        V = rng.standard_normal((seq, d))
+        out[f"{tag}.q"], out[f"{tag}.K"], out[f"{tag}.V"] = q, K, V
+        for n in (1, 2, 3, 4, 8, 16):
+            for sname, strat in strategies.items():
+                for prec in (Precision.EXACT, Precision.FP16):
+                    spec = ClusterSpec(n_blocks=n, reduction=strat, accumulation_precision=prec)
+                    with warnings.catch_warnings():
+                        warnings.simplefilter("ignore", RuntimeWarning)
+                        o, tr = attend_split(q, K, V, spec, 1.0 / np.sqrt(d))
+                    key = f"{tag}.n{n}.{sname}.{prec.value}"
+                    out[key + ".out"] = o
+                    r = tr.records[0]
+                    out[key + ".trace"] = np.array([r.bytes_offchip, r.bytes_onchip, r.sync_steps,
+                                                    r.dsmem_exchanges])
+    for hidden, n in ((64, 1), (64, 3), (96, 4), (128, 8), (80, 16)):
+        tag = f"h{hidden}n{n}"
+        P = rng.standard_normal((n, hidden)) * 2.0
+        W = rng.standard_normal((hidden, hidden)) * 0.3
+        b = rng.standard_normal(hidden) * 0.5
+        res = rng.standard_normal(hidden) * 4.0
+        out[f"{tag}.P"], out[f"{tag}.W"], out[f"{tag}.b"], out[f"{tag}.res"] = P, W, b, res
+        for prec in (Precision.EXACT, Precision.FP16):
+            for seed in (0, 5, 2**40 + 3):
+                spec = ClusterSpec(n_blocks=n, accumulation_precision=prec, atomic_seed=seed)
+                out[f"{tag}.{prec.value}.{seed}"] = output_project_atomic(P, W, b, res, spec)
+    np.savez(OUT / "split.npz", **out)
+
+
+ALL = [cli_fixture, prng, half, synth, blocks, fidelity, bytes_model, prefill, split]
 
 if __name__ == "__main__":
     # python tests/golden/make_golden.py [name ...]  (default: every fixture)
