@@ -252,8 +252,9 @@ __global__ void __launch_bounds__(kTile) attn_tile_kernel(const float* q, const 
         o8[2 * k + 1] = fmaf(pw2, f.y, o8[2 * k + 1]);
       }
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) so[grp * d + 8 * c8 + k] = o8[k];
+    float4* sv = reinterpret_cast<float4*>(so + grp * d + 8 * c8);  // two 16-byte stores (2-way, not 8-way, conflicts)
+    sv[0] = make_float4(o8[0], o8[1], o8[2], o8[3]);
+    sv[1] = make_float4(o8[4], o8[5], o8[6], o8[7]);
   }
   __syncthreads();
   for (int j = tid; j < d; j += blockDim.x) {
