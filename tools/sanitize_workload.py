@@ -48,6 +48,18 @@ def main():
         print("batch forward", hb.shape)
         hp = eng.prefill(18, rng.standard_normal((5, 768)) * 0.5)
         print("prefill", np.asarray(hp).shape)
+    # the reference's unit-level helpers on the GPU (csrc/nfb_split.cu)
+    from paper_2604_23553_b200 import cluster as cl
+    q, K, V = rng.standard_normal(80), rng.standard_normal((37, 80)), rng.standard_normal((37, 80))
+    for red in (cl.RING, cl.TREE, cl.ReductionStrategy(cl.ReductionKind.PERMUTED_ATOMIC, 7)):
+        for n in (1, 4, 64):
+            o, _ = cl.attend_split(q, K, V, cl.ClusterSpec(n_blocks=n, reduction=red,
+                                                           accumulation_precision=cl.Precision.FP16), 0.1)
+            assert np.all(np.isfinite(o))
+    y = cl.output_project_atomic(rng.standard_normal((4, 96)), rng.standard_normal((96, 96)), rng.standard_normal(96),
+                                 rng.standard_normal(96), cl.ClusterSpec(n_blocks=4, accumulation_precision=cl.Precision.FP16,
+                                                                         atomic_seed=3))
+    print("split helpers", y.shape)
     print("sanitize workload done")
 
 
