@@ -324,7 +324,7 @@ struct nfb_ctx {
   // independent); forked / joined with events (graph-capturable)
   cudaStream_t bstream2 = nullptr;
   cudaEvent_t bev[2] = {nullptr, nullptr};
-  int bfork = 1;
+  int bfork = 4;  // fork point of the MLP branch (batch_token); 0 = one stream
   int bskip = 0;  // measurement only (NFB_BATCH_SKIP, results garbage): 1 MLP branch, 2 attention, 4 GEMMs
   // stream-K partials per GEMM role [qkv, out, up, down, lm] (the consumer
   // kernels sum the pieces) and the plans of the current batch
@@ -1619,6 +1619,10 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     uint16_t* const* bw = &c->bw[(size_t)4 * l];
     CK(launch_pdl(ln_hilo_kernel, dim3(B), dim3(256), 0, st, c->bx, B, h, (float)m.ln_eps, w.ln1g, w.ln1b, w.ln2g,
                   w.ln2b, a1, a2, np));
+    // The MLP branch forks right after the LNs (bfork 4, default: the up GEMM
+    // streams beside the QKV GEMM -- both are latency-dominated at small B;
+    // C4 B = 2 / 4 / 16: +1.4 / +3 / +0.8 %) or after the QKV GEMM (bfork 1).
+    if (c->bfork == 4) CK(cudaEventRecord(c->bev[0], st));
     if (!(c->bskip & 4)) TRY(ugemm(c, st, 0, bw[0], a1));
     // batch: sequence b has its own cache; prefill: the T prompt rows share
     // the context's cache at consecutive positions (causal)
@@ -1629,7 +1633,7 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     // MLP branch (independent of the attention under the parallel residual)
     cudaStream_t sm = st;
     if (c->bfork) {
-      CK(cudaEventRecord(c->bev[0], st));
+      if (c->bfork != 4) CK(cudaEventRecord(c->bev[0], st));
       CK(cudaStreamWaitEvent(c->bstream2, c->bev[0], 0));
       sm = c->bstream2;
     }
