@@ -33,6 +33,10 @@ __global__ void attn_tile_kernel(const float* q, const __half* kc, const __half*
                                  size_t seq_stride);
 size_t attn_tile_smem(int d);
 int attn_tile_positions();
+int attn_prefill_rows();
+size_t attn_tile_rows_smem(int d);
+__global__ void attn_tile_rows_kernel(const float* q, const __half* kc, const __half* vc, int T, int H, int d,
+                                      int max_seq, const int* state, float scale_log2, float* part);
 // tcgen05 GEMM (csrc/nfb_umma.cu)
 UPlan umma_plan(int M, int N, int K, int sm_count);
 size_t umma_blocked_elems(int M, int K);
@@ -324,6 +328,7 @@ struct nfb_ctx {
   // independent); forked / joined with events (graph-capturable)
   cudaStream_t bstream2 = nullptr;
   cudaEvent_t bev[2] = {nullptr, nullptr};
+  int bprefill_rows = 1;  // prefill attention: attn_tile_rows_kernel (NFB_PREFILL_ROWS=0: one row per block)
   int bfork = 4;  // fork point of the MLP branch (batch_token); 0 = one stream
   int bskip = 0;  // measurement only (NFB_BATCH_SKIP, results garbage): 1 MLP branch, 2 attention, 4 GEMMs
   // stream-K partials per GEMM role [qkv, out, up, down, lm] (the consumer
@@ -1647,7 +1652,12 @@ static int batch_token(nfb_ctx* c, cudaStream_t st, bool in_token, bool head, bo
     if (!(c->bskip & 2)) {
       CK(launch_pdl(attn_prep_kernel, dim3(B, H), dim3(128), (size_t)3 * d * 4, st, oq, B, H, d, m.rotary_dims,
                     c->bstate, c->max_seq, w.bqkv, c->rope, c->bq, kc, vc, pstep, sstride));
-      CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(attn_tile_positions()), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
+      if (prefill && c->bprefill_rows)  // one tile fetch per kPrefillRows prompt rows
+        CK(launch_pdl(attn_tile_rows_kernel, dim3(H * ((B + attn_prefill_rows() - 1) / attn_prefill_rows()), S),
+                      dim3(attn_tile_positions()), attn_tile_rows_smem(d), st, c->bq, kc, vc, B, H, d, c->max_seq,
+                      c->bstate, scale_log2, c->bpart));
+      else
+        CK(launch_pdl(attn_tile_kernel, dim3(B * H, S), dim3(attn_tile_positions()), attn_tile_smem(d), st, c->bq, kc, vc, B, H, d,
                     c->max_seq, c->bstate, scale_log2, c->bpart, pstep, sstride));
       CK(launch_pdl(attn_combine_kernel, dim3(B * H), dim3(128), 0, st, c->bpart, S, B, H, d, actx, np));
       if (!(c->bskip & 4)) TRY(ugemm(c, st, 1, bw[1], actx));
@@ -1683,6 +1693,11 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   c->bsplit = (c->max_seq + attn_tile_positions() - 1) / attn_tile_positions();
   if (c->bsplit > 256) return fail(NFB_EUNSUPPORTED, "batched decode needs max_seq <= 32768");
   {
+    const cudaError_t e2 = cudaFuncSetAttribute(attn_tile_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)attn_tile_rows_smem((int)d));
+    if (e2 != cudaSuccess) return fail(NFB_ECUDA, std::string("attn_tile_rows smem attribute: ") + cudaGetErrorString(e2));
+  }
+  {
     const cudaError_t e = cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)attn_tile_smem((int)d));
     if (e != cudaSuccess) return fail(NFB_ECUDA, std::string("attn_tile smem attribute: ") + cudaGetErrorString(e));
@@ -1711,6 +1726,7 @@ int nfb_batch_init(nfb_ctx* c, int max_batch) {
   for (auto& e : c->bev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (getenv("NFB_BATCH_FORK")) c->bfork = atoi(getenv("NFB_BATCH_FORK"));
   if (getenv("NFB_BATCH_SKIP")) c->bskip = atoi(getenv("NFB_BATCH_SKIP"));
+  if (getenv("NFB_PREFILL_ROWS")) c->bprefill_rows = atoi(getenv("NFB_PREFILL_ROWS"));
   // stream-K partials per role: tiles x pieces x n_pad x 128 (pieces depend
   // on M, K and the grid only; n_pad is largest at the largest batch)
   for (int j = 0; j < 5; ++j)

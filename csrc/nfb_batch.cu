@@ -268,6 +268,126 @@ __global__ void __launch_bounds__(kTile) attn_tile_kernel(const float* q, const 
   }
 }
 
+// Prefill variant (rows of one prompt chunk share the one cache, row r at
+// position pos + r, causal): grid (H * ceil(T / kPrefillRows), S), block 128
+// (4 warps).  The block bulk-copies its 128-position K / V tile ONCE for
+// kPrefillRows consecutive rows (attn_tile_kernel re-fetched the same tile
+// for every row of the chunk) and each warp scores whole rows on its own --
+// lane L takes positions L, L + 32, L + 64, L + 96 (scores, warp-shuffle max /
+// sum) and context elements L, L + 32, ... (P.V) -- so a row needs no block
+// barrier.  Row r sees positions < pos + r + 1; its (m, l, o[d]) state goes
+// to part in the layout attn_combine_kernel merges.
+constexpr int kPrefillRows = 16;
+__global__ void __launch_bounds__(kTile) attn_tile_rows_kernel(const float* q, const __half* kc, const __half* vc,
+                                                             int T, int H, int d, int max_seq, const int* state,
+                                                             float scale_log2, float* part) {
+  griddep_wait();
+  const int hh = blockIdx.x % H, r0 = (blockIdx.x / H) * kPrefillRows, s = blockIdx.y, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int r1 = min(T, r0 + kPrefillRows), pos = state[0], p0 = s * kTile;
+  const int nmax = min(kTile, pos + r1 - p0);  // positions the last row sees in this tile
+  if (nmax <= 0) {
+    if (tid < r1 - r0) {
+      float* out = part + ((size_t)((r0 + tid) * H + hh) * gridDim.y + s) * (d + 2);
+      out[d] = -INFINITY;
+      out[d + 1] = 0.f;
+    }
+    return;
+  }
+  extern __shared__ __align__(128) unsigned char tsm[];
+  __half* Ks = reinterpret_cast<__half*>(tsm);
+  __half* Vs = Ks + kTile * d;
+  float* sq = reinterpret_cast<float*>(Vs + kTile * d);  // [4 warps][128]: the warp's q row (d <= 128)
+  float* sp = sq + 4 * 128;                              // [4 warps][kTile] weights
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sp + 4 * kTile);
+  const size_t base = ((size_t)hh * max_seq + p0) * d;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = (uint32_t)(nmax * d * 2);
+    mbar_arrive_expect_tx(bar, 2 * bytes);
+    const uint64_t pol = policy_evict_first();
+    bulk_g2s(Ks, kc + base, bytes, bar, pol);
+    bulk_g2s(Vs, vc + base, bytes, bar, pol);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0, nullptr, 31);
+  const int cpr = d >> 3;
+  float* wq = sq + warp * 128;
+  float* wp = sp + warp * kTile;
+  for (int r = r0 + warp; r < r1; r += 4) {
+    const int n = min(kTile, pos + r + 1 - p0);
+    float* out = part + ((size_t)(r * H + hh) * gridDim.y + s) * (d + 2);
+    if (n <= 0) {
+      if (lane == 0) {
+        out[d] = -INFINITY;
+        out[d + 1] = 0.f;
+      }
+      continue;
+    }
+    for (int i = lane; i < d; i += 32) wq[i] = q[((size_t)r * H + hh) * d + i];
+    __syncwarp();
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < cpr; ++c) {
+      const float4 q0 = *reinterpret_cast<const float4*>(wq + 8 * c);
+      const float4 q1 = *reinterpret_cast<const float4*>(wq + 8 * c + 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 w = reinterpret_cast<const uint4*>(Ks + (size_t)(lane + 32 * k) * d)[c];
+        const __half2* hp = reinterpret_cast<const __half2*>(&w);
+        const float2 f0 = __half22float2(hp[0]), f1 = __half22float2(hp[1]);
+        const float2 f2 = __half22float2(hp[2]), f3 = __half22float2(hp[3]);
+        a[k] = fmaf(f0.x, q0.x, a[k]);
+        a[k] = fmaf(f0.y, q0.y, a[k]);
+        a[k] = fmaf(f1.x, q0.z, a[k]);
+        a[k] = fmaf(f1.y, q0.w, a[k]);
+        a[k] = fmaf(f2.x, q1.x, a[k]);
+        a[k] = fmaf(f2.y, q1.y, a[k]);
+        a[k] = fmaf(f3.x, q1.z, a[k]);
+        a[k] = fmaf(f3.y, q1.w, a[k]);
+      }
+    }
+    float sc[4], mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sc[k] = lane + 32 * k < n ? a[k] * scale_log2 : -INFINITY;
+      mx = fmaxf(mx, sc[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float l = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float pw = lane + 32 * k < n ? exp2f(sc[k] - mx) : 0.f;
+      wp[lane + 32 * k] = pw;
+      l += pw;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    __syncwarp();
+    float o4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) {
+      const float pw = wp[i];
+      const __half* vr = Vs + (size_t)i * d + lane;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (lane + 32 * u < d) o4[u] = fmaf(pw, __half2float(vr[32 * u]), o4[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lane + 32 * u < d) out[lane + 32 * u] = o4[u];
+    if (lane == 0) {
+      out[d] = mx;
+      out[d + 1] = l;
+    }
+    __syncwarp();  // wq / wp reused by the warp's next row
+  }
+}
+
+int attn_prefill_rows() { return kPrefillRows; }
+size_t attn_tile_rows_smem(int d) { return (size_t)2 * kTile * d * 2 + (size_t)(4 * 128 + 4 * kTile) * 4 + 16; }
+
 size_t attn_tile_smem(int d) { return (size_t)2 * kTile * d * 2 + (size_t)(d + kTile + 32 + 2) * 4 + 8 + 8; }
 
 // grid B * H, block 128: merge the S split states in split order -> ctx
