@@ -56,6 +56,16 @@ __device__ __forceinline__ float block_max(float v, float* sh) {
   return t;
 }
 
+// Packed fp32x2 FMA (sm_100 FFMA2): a * b + c element-wise.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  const unsigned long long ab = (unsigned long long)__float_as_uint(a.x) | ((unsigned long long)__float_as_uint(a.y) << 32);
+  const unsigned long long bb = (unsigned long long)__float_as_uint(b.x) | ((unsigned long long)__float_as_uint(b.y) << 32);
+  const unsigned long long cb = (unsigned long long)__float_as_uint(c.x) | ((unsigned long long)__float_as_uint(c.y) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(ab), "l"(bb), "l"(cb));
+  return make_float2(__uint_as_float((unsigned)d), __uint_as_float((unsigned)(d >> 32)));
+}
+
 // v -> blocked activation rows b (hi) and B + b (lo), column k
 __device__ __forceinline__ void put_hilo(__half* a, int b, int B, int n_pad, int k, float v) {
   const __half hv = __float2half_rn(v);
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(kTile) attn_tile_rows_kernel(const float* q, c
     }
     for (int i = lane; i < d; i += 32) wq[i] = q[((size_t)r * H + hh) * d + i];
     __syncwarp();
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    float2 a[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     for (int c = 0; c < cpr; ++c) {
       const float4 q0 = *reinterpret_cast<const float4*>(wq + 8 * c);
       const float4 q1 = *reinterpret_cast<const float4*>(wq + 8 * c + 4);
@@ -335,22 +345,16 @@ __global__ void __launch_bounds__(kTile) attn_tile_rows_kernel(const float* q, c
       for (int k = 0; k < 4; ++k) {
         const uint4 w = reinterpret_cast<const uint4*>(Ks + (size_t)(lane + 32 * k) * d)[c];
         const __half2* hp = reinterpret_cast<const __half2*>(&w);
-        const float2 f0 = __half22float2(hp[0]), f1 = __half22float2(hp[1]);
-        const float2 f2 = __half22float2(hp[2]), f3 = __half22float2(hp[3]);
-        a[k] = fmaf(f0.x, q0.x, a[k]);
-        a[k] = fmaf(f0.y, q0.y, a[k]);
-        a[k] = fmaf(f1.x, q0.z, a[k]);
-        a[k] = fmaf(f1.y, q0.w, a[k]);
-        a[k] = fmaf(f2.x, q1.x, a[k]);
-        a[k] = fmaf(f2.y, q1.y, a[k]);
-        a[k] = fmaf(f3.x, q1.z, a[k]);
-        a[k] = fmaf(f3.y, q1.w, a[k]);
+        a[k] = ffma2(__half22float2(hp[0]), make_float2(q0.x, q0.y), a[k]);
+        a[k] = ffma2(__half22float2(hp[1]), make_float2(q0.z, q0.w), a[k]);
+        a[k] = ffma2(__half22float2(hp[2]), make_float2(q1.x, q1.y), a[k]);
+        a[k] = ffma2(__half22float2(hp[3]), make_float2(q1.z, q1.w), a[k]);
       }
     }
     float sc[4], mx = -INFINITY;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      sc[k] = lane + 32 * k < n ? a[k] * scale_log2 : -INFINITY;
+      sc[k] = lane + 32 * k < n ? (a[k].x + a[k].y) * scale_log2 : -INFINITY;
       mx = fmaxf(mx, sc[k]);
     }
 #pragma unroll
@@ -365,18 +369,39 @@ __global__ void __launch_bounds__(kTile) attn_tile_rows_kernel(const float* q, c
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
     __syncwarp();
-    float o4[4] = {0.f, 0.f, 0.f, 0.f};
+    // P.V: lane = (context chunk c8 of 8 elements, position group g); the
+    // groups' partial sums are added in group order through shuffles
+    const int ngrp = 32 / cpr, c8 = lane % cpr, g = lane / cpr;
+    float2 o2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    if (g < ngrp) {
+      const uint4* vr = reinterpret_cast<const uint4*>(Vs) + c8;
 #pragma unroll 4
-    for (int i = 0; i < n; ++i) {
-      const float pw = wp[i];
-      const __half* vr = Vs + (size_t)i * d + lane;
+      for (int i = g; i < n; i += ngrp) {
+        const uint4 w = vr[(size_t)i * cpr];
+        const __half2* hp = reinterpret_cast<const __half2*>(&w);
+        const float2 pw2 = make_float2(wp[i], wp[i]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (lane + 32 * u < d) o4[u] = fmaf(pw, __half2float(vr[32 * u]), o4[u]);
+        for (int k = 0; k < 4; ++k) o2[k] = ffma2(pw2, __half22float2(hp[k]), o2[k]);
+      }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (lane + 32 * u < d) out[lane + 32 * u] = o4[u];
+    for (int k = 0; k < 4; ++k) {
+      float2 t = o2[k];
+      for (int gg = 1; gg < ngrp; ++gg) {
+        const float x = __shfl_sync(0xffffffffu, o2[k].x, min(31, lane + gg * cpr));
+        const float y = __shfl_sync(0xffffffffu, o2[k].y, min(31, lane + gg * cpr));
+        t.x += x;
+        t.y += y;
+      }
+      o2[k] = t;
+    }
+    if (g == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        out[8 * c8 + 2 * k] = o2[k].x;
+        out[8 * c8 + 2 * k + 1] = o2[k].y;
+      }
+    }
     if (lane == 0) {
       out[d] = mx;
       out[d + 1] = l;
