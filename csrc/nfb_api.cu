@@ -55,6 +55,10 @@ cudaError_t launch_decode(const Params& p, int dpl, int grid, int block, int sme
                           bool cooperative);
 cudaError_t max_active_clusters(int dpl, int C, int block, int smem, int* out);
 // single-head split-KV attention / atomic output projection (csrc/nfb_split.cu)
+cudaError_t golden_step(const GoldenBufs& B, const double* x, double* out, int h, int H, int d, int m, int rd,
+                        double eps, double base, int pos, int max_seq, int parallel, int gelu_exact,
+                        cudaStream_t st);
+cudaError_t golden_probe(const double* unembed, const double* hv, int vocab, int h, double* logits, cudaStream_t st);
 cudaError_t launch_attend_split(const double* q, const double* K, const double* V, int seq, int d, int n, int mode,
                                 uint64_t seed, double scale, double* logits, double* states, int* order,
                                 void* scratch, double* out, cudaStream_t st);
@@ -1958,6 +1962,70 @@ int nfb_attend_split(const double* q, const double* keys, const double* values, 
   const int mode = n_blocks == 1 ? 4 : merge;
   CK(launch_attend_split(dq, dk, dv, seq_len, d, n_blocks, mode, seed, scale, lg, st, ord, sc, o, nullptr));
   CK(cudaMemcpy(out, o, d * sizeof(double), cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+// DecodeInstance.golden_logits (nf/fidelity.py:131-140): the float64 golden
+// block (nf/golden.py:189-228) stepped over xs with a fresh cache from the
+// prompt K/V, logits = unembed @ h per step (csrc/nfb_golden.cu).
+int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const double* unembed, const double* xs,
+                      int steps, const double* prompt_k, const double* prompt_v, int prompt_len, double* logits) {
+  if (!m || !w || !unembed || !xs || !logits || (prompt_len > 0 && (!prompt_k || !prompt_v)))
+    return fail(NFB_EINVAL, "null argument");
+  const int h = m->hidden, H = m->n_heads, d = m->d_head, mm = m->d_mlp, V = m->vocab, rd = m->rotary_dims;
+  if (h < 1 || H < 1 || d < 1 || mm < 1 || V < 1 || H * d != h) return fail(NFB_EINVAL, "invalid model shape");
+  if (rd < 2 || rd % 2 || rd > d) return fail(NFB_EINVAL, "rotary_dims must be an even number >= 2 and <= d_head");
+  if (steps < 0 || prompt_len < 0) return fail(NFB_EINVAL, "steps and prompt_len must be >= 0");
+  if (steps == 0) return NFB_OK;
+  const int S = prompt_len + steps;
+  const size_t D = sizeof(double);
+  DevScratch s;
+  GoldenBufs B{};
+  double *wbuf[12], *dx, *dout, *dun, *dlg;
+  const size_t sizes[12] = {(size_t)h, (size_t)h, (size_t)3 * h * h, (size_t)3 * h, (size_t)h * h, (size_t)h,
+                            (size_t)h, (size_t)h, (size_t)mm * h, (size_t)mm, (size_t)h * mm, (size_t)h};
+  const void* src[12] = {w->ln1_gain, w->ln1_bias, w->qkv_weight, w->qkv_bias, w->out_weight, w->out_bias,
+                         w->ln2_gain, w->ln2_bias, w->up_weight, w->up_bias, w->down_weight, w->down_bias};
+  for (int i = 0; i < 12; ++i) {
+    if (!src[i]) return fail(NFB_EINVAL, "null weight tensor");
+    CK(s.get(&wbuf[i], sizes[i] * D));
+    CK(cudaMemcpy(wbuf[i], src[i], sizes[i] * D, cudaMemcpyHostToDevice));
+  }
+  B.ln1g = wbuf[0]; B.ln1b = wbuf[1]; B.wqkv = wbuf[2]; B.bqkv = wbuf[3]; B.wo = wbuf[4]; B.bo = wbuf[5];
+  B.ln2g = wbuf[6]; B.ln2b = wbuf[7]; B.wup = wbuf[8]; B.bup = wbuf[9]; B.wdown = wbuf[10]; B.bdown = wbuf[11];
+  CK(s.get(&B.kc, (size_t)H * S * d * D));
+  CK(s.get(&B.vc, (size_t)H * S * d * D));
+  CK(s.get(&B.n1, h * D));
+  CK(s.get(&B.y, 3 * (size_t)h * D));
+  CK(s.get(&B.q, h * D));
+  CK(s.get(&B.lg, (size_t)H * S * D));
+  CK(s.get(&B.ctx, h * D));
+  CK(s.get(&B.attn, h * D));
+  CK(s.get(&B.n2, h * D));
+  CK(s.get(&B.act, mm * D));
+  CK(s.get(&B.bad, sizeof(int)));
+  CK(s.get(&dx, (size_t)steps * h * D));
+  CK(s.get(&dout, h * D));
+  CK(s.get(&dun, (size_t)V * h * D));
+  CK(s.get(&dlg, (size_t)steps * V * D));
+  CK(cudaMemset(B.bad, 0, sizeof(int)));
+  CK(cudaMemcpy(dx, xs, (size_t)steps * h * D, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dun, unembed, (size_t)V * h * D, cudaMemcpyHostToDevice));
+  for (int hh = 0; hh < H && prompt_len > 0; ++hh) {  // prompt K (already rotated) / V -> [H][S][d]
+    CK(cudaMemcpy(B.kc + (size_t)hh * S * d, prompt_k + (size_t)hh * prompt_len * d, (size_t)prompt_len * d * D,
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(B.vc + (size_t)hh * S * d, prompt_v + (size_t)hh * prompt_len * d, (size_t)prompt_len * d * D,
+                  cudaMemcpyHostToDevice));
+  }
+  for (int t = 0; t < steps; ++t) {
+    CK(golden_step(B, dx + (size_t)t * h, dout, h, H, d, mm, rd, m->ln_eps, m->theta_base, prompt_len + t, S,
+                   m->parallel_residual, m->gelu_exact, nullptr));
+    CK(golden_probe(dun, dout, V, h, dlg + (size_t)t * V, nullptr));
+  }
+  int bad = 0;
+  CK(cudaMemcpy(&bad, B.bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) return fail(NFB_EINVAL, "non-finite activation");
+  CK(cudaMemcpy(logits, dlg, (size_t)steps * V * D, cudaMemcpyDeviceToHost));
   return NFB_OK;
 }
 

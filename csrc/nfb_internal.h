@@ -168,4 +168,13 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   return L;
 }
 
+// Device work buffers of the float64 golden block (csrc/nfb_golden.cu).
+struct GoldenBufs {
+  const double *ln1g, *ln1b, *wqkv, *bqkv, *wo, *bo, *ln2g, *ln2b, *wup, *bup, *wdown, *bdown;
+  double *kc, *vc;                // [H][max_seq][d]
+  double *n1, *y, *q, *lg, *ctx;  // scratch
+  double *attn, *n2, *act;        // attn_res [h], normed2 [h], gelu(up) [m]
+  int* bad;                       // set on a non-finite LayerNorm input
+};
+
 }  // namespace nfb

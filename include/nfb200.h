@@ -263,6 +263,21 @@ int nfb_output_project_atomic(const double* partials, const double* w_out, const
                               const double* residual, int n_blocks, int hidden, int fp16, uint64_t seed,
                               double* out);
 
+/* nfb_golden_logits replaces neoxfuse.fidelity.DecodeInstance.golden_logits
+ * (nf/fidelity.py:131-140): the float64 golden block decoder_block_golden
+ * (nf/golden.py:189-228; weights used as given, two-pass LayerNorm, naive
+ * per-head softmax over the cache incl. the fresh token) stepped over
+ * xs[steps][hidden] from a fresh cache holding prompt_k / prompt_v
+ * [n_heads][prompt_len][d_head] (keys already rotated), logits[steps][vocab] =
+ * unembed[vocab][hidden] @ h per step.  Model from `m` (n_layers ignored;
+ * gelu_exact, parallel_residual, ln_eps, theta_base, rotary_dims used);
+ * float64 host arrays, weights in the reference [out, in] shapes; runs on the
+ * current device in float64 (csrc/nfb_golden.cu), synchronous.  A non-finite
+ * LayerNorm input returns NFB_EINVAL "non-finite activation"
+ * (nf/golden.py:29-31). */
+int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const double* unembed, const double* xs,
+                      int steps, const double* prompt_k, const double* prompt_v, int prompt_len, double* logits);
+
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
 
