@@ -1965,23 +1965,14 @@ int nfb_attend_split(const double* q, const double* keys, const double* values, 
   return NFB_OK;
 }
 
-// DecodeInstance.golden_logits (nf/fidelity.py:131-140): the float64 golden
-// block (nf/golden.py:189-228) stepped over xs with a fresh cache from the
-// prompt K/V, logits = unembed @ h per step (csrc/nfb_golden.cu).
-int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const double* unembed, const double* xs,
-                      int steps, const double* prompt_k, const double* prompt_v, int prompt_len, double* logits) {
-  if (!m || !w || !unembed || !xs || !logits || (prompt_len > 0 && (!prompt_k || !prompt_v)))
-    return fail(NFB_EINVAL, "null argument");
+// Float64 golden block on the GPU (csrc/nfb_golden.cu): shape checks, weight
+// upload and work buffers for a cache of S positions.
+static int golden_setup(const nfb_model_desc* m, const nfb_block_weights* w, int S, DevScratch& s, GoldenBufs& B) {
   const int h = m->hidden, H = m->n_heads, d = m->d_head, mm = m->d_mlp, V = m->vocab, rd = m->rotary_dims;
   if (h < 1 || H < 1 || d < 1 || mm < 1 || V < 1 || H * d != h) return fail(NFB_EINVAL, "invalid model shape");
   if (rd < 2 || rd % 2 || rd > d) return fail(NFB_EINVAL, "rotary_dims must be an even number >= 2 and <= d_head");
-  if (steps < 0 || prompt_len < 0) return fail(NFB_EINVAL, "steps and prompt_len must be >= 0");
-  if (steps == 0) return NFB_OK;
-  const int S = prompt_len + steps;
   const size_t D = sizeof(double);
-  DevScratch s;
-  GoldenBufs B{};
-  double *wbuf[12], *dx, *dout, *dun, *dlg;
+  double* wbuf[12];
   const size_t sizes[12] = {(size_t)h, (size_t)h, (size_t)3 * h * h, (size_t)3 * h, (size_t)h * h, (size_t)h,
                             (size_t)h, (size_t)h, (size_t)mm * h, (size_t)mm, (size_t)h * mm, (size_t)h};
   const void* src[12] = {w->ln1_gain, w->ln1_bias, w->qkv_weight, w->qkv_bias, w->out_weight, w->out_bias,
@@ -2004,28 +1995,87 @@ int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const
   CK(s.get(&B.n2, h * D));
   CK(s.get(&B.act, mm * D));
   CK(s.get(&B.bad, sizeof(int)));
+  CK(cudaMemset(B.bad, 0, sizeof(int)));
+  return NFB_OK;
+}
+
+// history [H][len][d] (host) -> positions [0, len) of the [H][S][d] device cache
+static int golden_load_cache(const GoldenBufs& B, const double* keys, const double* values, int H, int len, int S,
+                             int d) {
+  const size_t D = sizeof(double);
+  for (int hh = 0; hh < H && len > 0; ++hh) {
+    CK(cudaMemcpy(B.kc + (size_t)hh * S * d, keys + (size_t)hh * len * d, (size_t)len * d * D,
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(B.vc + (size_t)hh * S * d, values + (size_t)hh * len * d, (size_t)len * d * D,
+                  cudaMemcpyHostToDevice));
+  }
+  return NFB_OK;
+}
+
+static int golden_check_finite(const GoldenBufs& B) {
+  int bad = 0;
+  CK(cudaMemcpy(&bad, B.bad, sizeof(int), cudaMemcpyDeviceToHost));
+  return bad ? fail(NFB_EINVAL, "non-finite activation") : NFB_OK;
+}
+
+// DecodeInstance.golden_logits (nf/fidelity.py:131-140): the float64 golden
+// block (nf/golden.py:189-228) stepped over xs with a fresh cache from the
+// prompt K/V, logits = unembed @ h per step (csrc/nfb_golden.cu).
+int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const double* unembed, const double* xs,
+                      int steps, const double* prompt_k, const double* prompt_v, int prompt_len, double* logits) {
+  if (!m || !w || !unembed || !xs || !logits || (prompt_len > 0 && (!prompt_k || !prompt_v)))
+    return fail(NFB_EINVAL, "null argument");
+  if (steps < 0 || prompt_len < 0) return fail(NFB_EINVAL, "steps and prompt_len must be >= 0");
+  if (steps == 0) return NFB_OK;
+  const int h = m->hidden, H = m->n_heads, d = m->d_head, V = m->vocab, S = prompt_len + steps;
+  const size_t D = sizeof(double);
+  DevScratch s;
+  GoldenBufs B{};
+  TRY(golden_setup(m, w, S, s, B));
+  double *dx, *dout, *dun, *dlg;
   CK(s.get(&dx, (size_t)steps * h * D));
   CK(s.get(&dout, h * D));
   CK(s.get(&dun, (size_t)V * h * D));
   CK(s.get(&dlg, (size_t)steps * V * D));
-  CK(cudaMemset(B.bad, 0, sizeof(int)));
   CK(cudaMemcpy(dx, xs, (size_t)steps * h * D, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dun, unembed, (size_t)V * h * D, cudaMemcpyHostToDevice));
-  for (int hh = 0; hh < H && prompt_len > 0; ++hh) {  // prompt K (already rotated) / V -> [H][S][d]
-    CK(cudaMemcpy(B.kc + (size_t)hh * S * d, prompt_k + (size_t)hh * prompt_len * d, (size_t)prompt_len * d * D,
-                  cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(B.vc + (size_t)hh * S * d, prompt_v + (size_t)hh * prompt_len * d, (size_t)prompt_len * d * D,
-                  cudaMemcpyHostToDevice));
-  }
+  TRY(golden_load_cache(B, prompt_k, prompt_v, H, prompt_len, S, d));
   for (int t = 0; t < steps; ++t) {
-    CK(golden_step(B, dx + (size_t)t * h, dout, h, H, d, mm, rd, m->ln_eps, m->theta_base, prompt_len + t, S,
-                   m->parallel_residual, m->gelu_exact, nullptr));
+    CK(golden_step(B, dx + (size_t)t * h, dout, h, H, d, m->d_mlp, m->rotary_dims, m->ln_eps, m->theta_base,
+                   prompt_len + t, S, m->parallel_residual, m->gelu_exact, nullptr));
     CK(golden_probe(dun, dout, V, h, dlg + (size_t)t * V, nullptr));
   }
-  int bad = 0;
-  CK(cudaMemcpy(&bad, B.bad, sizeof(int), cudaMemcpyDeviceToHost));
-  if (bad) return fail(NFB_EINVAL, "non-finite activation");
+  TRY(golden_check_finite(B));
   CK(cudaMemcpy(logits, dlg, (size_t)steps * V * D, cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+// decoder_block_golden (nf/golden.py:189-228): one float64 golden step at
+// pos = len over the history keys / values [H][len][d]; out [h], and the
+// step's rotated K and V [H][d] for the caller's cache append.
+int nfb_golden_block_step(const nfb_model_desc* m, const nfb_block_weights* w, const double* x, const double* keys,
+                          const double* values, int len, double* out, double* k_new, double* v_new) {
+  if (!m || !w || !x || !out || !k_new || !v_new || (len > 0 && (!keys || !values)))
+    return fail(NFB_EINVAL, "null argument");
+  if (len < 0) return fail(NFB_EINVAL, "len must be >= 0");
+  const int h = m->hidden, H = m->n_heads, d = m->d_head, S = len + 1;
+  const size_t D = sizeof(double);
+  DevScratch s;
+  GoldenBufs B{};
+  TRY(golden_setup(m, w, S, s, B));
+  double *dx, *dout;
+  CK(s.get(&dx, h * D));
+  CK(s.get(&dout, h * D));
+  CK(cudaMemcpy(dx, x, h * D, cudaMemcpyHostToDevice));
+  TRY(golden_load_cache(B, keys, values, H, len, S, d));
+  CK(golden_step(B, dx, dout, h, H, d, m->d_mlp, m->rotary_dims, m->ln_eps, m->theta_base, len, S,
+                 m->parallel_residual, m->gelu_exact, nullptr));
+  TRY(golden_check_finite(B));
+  CK(cudaMemcpy(out, dout, h * D, cudaMemcpyDeviceToHost));
+  for (int hh = 0; hh < H; ++hh) {
+    CK(cudaMemcpy(k_new + (size_t)hh * d, B.kc + ((size_t)hh * S + len) * d, d * D, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(v_new + (size_t)hh * d, B.vc + ((size_t)hh * S + len) * d, d * D, cudaMemcpyDeviceToHost));
+  }
   return NFB_OK;
 }
 

@@ -277,6 +277,14 @@ int nfb_output_project_atomic(const double* partials, const double* w_out, const
  * (nf/golden.py:29-31). */
 int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const double* unembed, const double* xs,
                       int steps, const double* prompt_k, const double* prompt_v, int prompt_len, double* logits);
+/* nfb_golden_block_step replaces neoxfuse.golden.decoder_block_golden
+ * (nf/golden.py:189-228): one float64 golden step of the block at pos = len
+ * over the history keys / values [n_heads][len][d_head] (float64, keys
+ * rotated); out[hidden] and the step's rotated key / value k_new, v_new
+ * [n_heads][d_head] for the caller's cache append.  Same model fields,
+ * device and errors as nfb_golden_logits. */
+int nfb_golden_block_step(const nfb_model_desc* m, const nfb_block_weights* w, const double* x, const double* keys,
+                          const double* values, int len, double* out, double* k_new, double* v_new);
 
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);
