@@ -59,6 +59,8 @@ cudaError_t golden_step(const GoldenBufs& B, const double* x, double* out, int h
                         double eps, double base, int pos, int max_seq, int parallel, int gelu_exact,
                         cudaStream_t st);
 cudaError_t golden_probe(const double* unembed, const double* hv, int vocab, int h, double* logits, cudaStream_t st);
+cudaError_t golden_prefill_tiled(const double* Q, const double* K, const double* V, int seq, int d, int tile,
+                                 int causal, double scale, double* out, cudaStream_t st);
 cudaError_t launch_attend_split(const double* q, const double* K, const double* V, int seq, int d, int n, int mode,
                                 uint64_t seed, double scale, double* logits, double* states, int* order,
                                 void* scratch, double* out, cudaStream_t st);
@@ -2047,6 +2049,31 @@ int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const
   }
   TRY(golden_check_finite(B));
   CK(cudaMemcpy(logits, dlg, (size_t)steps * V * D, cudaMemcpyDeviceToHost));
+  return NFB_OK;
+}
+
+// prefill_attention_tiled (nf/golden.py:234-265) for one head: Q, K, V
+// [seq][d] float64 host arrays -> out [seq][d].
+int nfb_prefill_attention_tiled(const double* Q, const double* K, const double* V, int seq, int d, int tile,
+                                int causal, double scale, double* out) {
+  if (!Q || !K || !V || !out) return fail(NFB_EINVAL, "null argument");
+  if (seq < 0 || d < 1) return fail(NFB_EINVAL, "Q, K, V must share shape [seq, d_head]");
+  if (tile < 1) return fail(NFB_EINVAL, "tile must be >= 1");
+  if (seq == 0) return NFB_OK;
+  const int t = tile < seq ? tile : seq;  // a tile wider than the sequence is the whole sequence
+  if (((size_t)t + d) * sizeof(double) > 200 * 1024) return fail(NFB_EINVAL, "tile too large for shared memory");
+  const size_t bytes = (size_t)seq * d * sizeof(double);
+  DevScratch s;
+  double *dq, *dk, *dv, *o;
+  CK(s.get(&dq, bytes));
+  CK(s.get(&dk, bytes));
+  CK(s.get(&dv, bytes));
+  CK(s.get(&o, bytes));
+  CK(cudaMemcpy(dq, Q, bytes, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dk, K, bytes, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dv, V, bytes, cudaMemcpyHostToDevice));
+  CK(golden_prefill_tiled(dq, dk, dv, seq, d, t, causal ? 1 : 0, scale, o, nullptr));
+  CK(cudaMemcpy(out, o, bytes, cudaMemcpyDeviceToHost));
   return NFB_OK;
 }
 

@@ -154,7 +154,68 @@ __global__ void __launch_bounds__(256) attend_kernel(const double* q, const doub
   }
 }
 
+// prefill_attention_tiled (nf/golden.py:234-265), one block per query row i:
+// keys [0, limit) (limit = i + 1 causal, else seq) consumed in tiles of
+// `tile` positions, each tile's two-pass softmax state (nf/golden.py:113-122)
+// merged into the row's running state with the log-sum-exp rule
+// (nf/golden.py:125-134; an empty running state takes the tile's as is).
+// Dynamic shared memory: the tile's logits (tile doubles) + o [d].
+__global__ void __launch_bounds__(128) prefill_tiled_kernel(const double* Q, const double* K, const double* V,
+                                                            int seq, int d, int tile, int causal, double scale,
+                                                            double* out) {
+  extern __shared__ double psm[];
+  __shared__ double sh[32];
+  double* lg = psm;         // [tile]
+  double* o = psm + tile;   // [d] running weighted values
+  const int i = blockIdx.x, limit = causal ? i + 1 : seq;
+  const double* q = Q + (size_t)i * d;
+  double m = -INFINITY, l = 0.0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) o[j] = 0.0;
+  for (int t0 = 0; t0 < limit; t0 += tile) {
+    const int t1 = min(t0 + tile, limit);
+    double mx = -INFINITY;
+    for (int p = t0 + threadIdx.x; p < t1; p += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += K[(size_t)p * d + j] * q[j];
+      s *= scale;
+      lg[p - t0] = s;
+      mx = fmax(mx, s);
+    }
+    const double mt = block_max_g(mx, sh);
+    double t = 0.0;
+    for (int p = t0 + threadIdx.x; p < t1; p += blockDim.x) {
+      const double e = exp(lg[p - t0] - mt);
+      lg[p - t0] = e;
+      t += e;
+    }
+    const double lt = block_sum_g(t, sh);  // (barriers: the weights are visible below)
+    const double M = l == 0.0 ? mt : fmax(m, mt);
+    const double fa = l == 0.0 ? 0.0 : exp(m - M), fb = l == 0.0 ? 1.0 : exp(mt - M);
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      double ot = 0.0;
+      for (int p = t0; p < t1; ++p) ot += lg[p - t0] * V[(size_t)p * d + j];
+      o[j] = l == 0.0 ? ot : o[j] * fa + ot * fb;
+    }
+    l = l == 0.0 ? lt : l * fa + lt * fb;
+    m = M;
+    __syncthreads();  // lg reused by the next tile
+  }
+  for (int j = threadIdx.x; j < d; j += blockDim.x) out[(size_t)i * d + j] = o[j] / l;
+}
+
 }  // namespace
+
+cudaError_t golden_prefill_tiled(const double* Q, const double* K, const double* V, int seq, int d, int tile,
+                                 int causal, double scale, double* out, cudaStream_t st) {
+  const size_t smem = ((size_t)tile + d) * sizeof(double);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(prefill_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  prefill_tiled_kernel<<<seq, 128, smem, st>>>(Q, K, V, seq, d, tile, causal, scale, out);
+  return cudaGetLastError();
+}
 
 // One decoder_block_golden step (nf/golden.py:189-228) on device vectors:
 // x [h] -> out [h]; the cache holds positions < pos and gains pos.

@@ -285,6 +285,13 @@ int nfb_golden_logits(const nfb_model_desc* m, const nfb_block_weights* w, const
  * device and errors as nfb_golden_logits. */
 int nfb_golden_block_step(const nfb_model_desc* m, const nfb_block_weights* w, const double* x, const double* keys,
                           const double* values, int len, double* out, double* k_new, double* v_new);
+/* nfb_prefill_attention_tiled replaces neoxfuse.golden.prefill_attention_tiled
+ * (nf/golden.py:234-265): one head, Q, K, V [seq][d_head] float64; each query
+ * row folds its keys [0, i] (causal != 0) or [0, seq) in tiles of `tile`
+ * positions into a running softmax state; out [seq][d_head].  float64 on the
+ * current device (csrc/nfb_golden.cu), synchronous. */
+int nfb_prefill_attention_tiled(const double* Q, const double* K, const double* V, int seq, int d, int tile,
+                                int causal, double scale, double* out);
 
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* nfb_stream(nfb_ctx* ctx);

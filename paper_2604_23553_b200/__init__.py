@@ -15,7 +15,7 @@ from .cluster import (
 )
 from .config import PRESETS, ModelConfig, preset
 from .engine import Engine, kv_seed
-from .golden import decoder_block_golden
+from .golden import decoder_block_golden, prefill_attention_tiled
 from .fidelity import (
     ADVERSARIAL_N_BLOCKS, DecodeInstance, FidelityReport, SweepSummary, adversarial_instance,
     compare, distinct_greedy_outputs, format_report, greedy_tokens, seed_sweep, synthetic_instance, topk_indices,

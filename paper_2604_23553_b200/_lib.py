@@ -107,6 +107,7 @@ SIGNATURES = {
     "nfb_output_project_atomic": (_I, [_P, _P, _P, _P, _I, _I, _I, C.c_uint64, _P]),
     "nfb_golden_logits": (_I, [C.POINTER(ModelDesc), C.POINTER(BlockWeightPtrs), _P, _P, _I, _P, _P, _I, _P]),
     "nfb_golden_block_step": (_I, [C.POINTER(ModelDesc), C.POINTER(BlockWeightPtrs), _P, _P, _P, _I, _P, _P, _P]),
+    "nfb_prefill_attention_tiled": (_I, [_P, _P, _P, _I, _I, _I, _I, C.c_double, _P]),
 }
 
 _lib = None

@@ -14,6 +14,7 @@ bitwise.
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import numpy as np
 
@@ -77,4 +78,27 @@ def golden_logits(cfg, w, unembed, xs, prompt_keys, prompt_values, gelu: str = "
     _lib.check(lib.nfb_golden_logits(C.byref(desc), C.byref(ptrs), _lib.vptr(un), _lib.vptr(xs), xs.shape[0],
                                      _lib.vptr(pk), _lib.vptr(pv), pk.shape[1], _lib.vptr(out)), "golden_logits")
     del keep
+    return out
+
+
+def prefill_attention_tiled(Q, K, V, tile: int, causal: bool = True, scale: float | None = None) -> np.ndarray:
+    """Causal (or full) attention of one head over whole sequences, keys folded
+    in tiles of ``tile`` positions into a running softmax state per query row
+    (nf/golden.py:234-265), in float64 on the GPU
+    (``nfb_prefill_attention_tiled``).  Q, K, V: [seq, d_head]."""
+    Q, K, V = _f64(Q), _f64(K), _f64(V)
+    if Q.ndim != 2 or K.shape != Q.shape or V.shape != Q.shape:
+        raise ValueError("Q, K, V must share shape [seq, d_head]")
+    if tile < 1:
+        raise ValueError("tile must be >= 1")
+    seq, d = Q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    out = np.empty((seq, d))
+    if seq == 0:
+        return out
+    lib = _lib.load()
+    _lib.check(lib.nfb_prefill_attention_tiled(_lib.vptr(Q), _lib.vptr(K), _lib.vptr(V), seq, d, int(tile),
+                                               1 if causal else 0, float(scale), _lib.vptr(out)),
+               "prefill_attention_tiled")
     return out
