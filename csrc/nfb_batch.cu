@@ -213,14 +213,18 @@ __global__ void __launch_bounds__(kTile) attn_tile_kernel(const float* q, const 
   float* so = reinterpret_cast<float*>(Ks);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sh + 32 + 2);
   const size_t base = (size_t)(bh / H) * seq_stride + ((size_t)(bh % H) * max_seq + p0) * d;
+  // K and V on separate mbarriers: the scores start when K has landed
+  // while V is still in flight
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
     const uint32_t bytes = (uint32_t)(n * d * 2);
-    mbar_arrive_expect_tx(bar, 2 * bytes);
+    mbar_arrive_expect_tx(bar, bytes);
+    mbar_arrive_expect_tx(bar + 1, bytes);
     const uint64_t pol = policy_evict_first();
     bulk_g2s(Ks, kc + base, bytes, bar, pol);
-    bulk_g2s(Vs, vc + base, bytes, bar, pol);
+    bulk_g2s(Vs, vc + base, bytes, bar + 1, pol);
   }
   for (int i = tid; i < d; i += blockDim.x) sq[i] = q[(size_t)bh * d + i];
   __syncthreads();
@@ -247,6 +251,7 @@ __global__ void __launch_bounds__(kTile) attn_tile_kernel(const float* q, const 
   sp[tid] = pw;
   const float l = block_sum(pw, sh);  // (syncs: sp is visible below)
   const int ng = blockDim.x / cpr, c8 = tid % cpr, grp = tid / cpr;
+  mbar_wait(bar + 1, 0, nullptr, 30);
   if (grp < ng) {
     float o8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const uint4* vr = reinterpret_cast<const uint4*>(Vs) + c8;
