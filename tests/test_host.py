@@ -184,3 +184,36 @@ def test_gemm_stream_k_plan(M, N, K):
         worst = max(worst, len(pieces))
     assert worst == max_pieces
     assert lib.nfb_gemm_plan(M, 0, K, 148, out) < 0
+
+
+def test_golden_entries_reject_bad_arguments_before_touching_the_gpu():
+    """The float64 golden entries (nfb_golden_*, nfb_prefill_attention_tiled)
+    validate like the reference (nf/golden.py:80-84, 189-205, 234-255) before
+    any device work, so the checks run here without a GPU."""
+    cfg = pkg.preset("tiny")
+    w = pkg.synth_weights(cfg, 1)
+    cache = pkg.KVCache(cfg.n_heads, cfg.d_head)
+    x = np.zeros(cfg.hidden)
+    with pytest.raises(ValueError, match=r"input must have shape"):
+        pkg.decoder_block_golden(x[:-1], w, cache, 0, cfg)
+    with pytest.raises(ValueError, match="cache holds 0 positions, expected 3"):
+        pkg.decoder_block_golden(x, w, cache, 3, cfg)
+    with pytest.raises(ValueError, match="unknown gelu variant"):
+        pkg.decoder_block_golden(x, w, cache, 0, cfg, gelu="relu")
+    q = np.zeros((5, 8))
+    with pytest.raises(ValueError, match="tile must be >= 1"):
+        pkg.prefill_attention_tiled(q, q, q, 0)
+    with pytest.raises(ValueError, match="must share shape"):
+        pkg.prefill_attention_tiled(q, q[:4], q, 2)
+    # C-ABI level: an odd rotary width is rejected with the reference's message
+    lib = _lib.load()
+    desc = _lib.ModelDesc(cfg.hidden, cfg.n_heads, cfg.d_head, 1, cfg.d_mlp, 3, cfg.vocab, 1e-5, 1e4, 1, 0)
+    arrs = [np.ascontiguousarray(getattr(w, n), dtype=np.float64) for n in pkg.TENSOR_NAMES]
+    ptrs = _lib.BlockWeightPtrs(*[a.ctypes.data for a in arrs])
+    out = np.empty(cfg.hidden)
+    kn = np.empty((cfg.n_heads, cfg.d_head))
+    rc = lib.nfb_golden_block_step(ctypes.byref(desc), ctypes.byref(ptrs), _lib.vptr(x), None, None, 0,
+                                   _lib.vptr(out), _lib.vptr(kn), _lib.vptr(kn))
+    assert rc == _lib.NFB_EINVAL and b"rotary_dims" in lib.nfb_last_error()
+    assert lib.nfb_prefill_attention_tiled(_lib.vptr(q), _lib.vptr(q), _lib.vptr(q), 5, 8, 0, 1, 1.0,
+                                           _lib.vptr(q)) == _lib.NFB_EINVAL
