@@ -1595,7 +1595,16 @@ static int batch_prepare(nfb_ctx* c, cudaStream_t st) {
   }
   if (c->uplan_rows != c->bcur) {
     const int shapes[5][2] = {{3 * h, h}, {h, h}, {mm, h}, {h, mm}, {V, h}};
-    for (int j = 0; j < 5; ++j) c->uplan[j] = umma_plan(shapes[j][0], 2 * c->bcur, shapes[j][1], c->sm_count);
+    // The MLP branch's GEMMs (up, down) run beside the attention branch; at
+    // B <= 8 they get one CTA per SM instead of 1.5, leaving the extra slots
+    // to the critical attention chain (C4 B = 2 / 3 / 4 / 8: +2.9 / +3.0 /
+    // +2.7 / +1.5 %; B = 16: -2.4 %, so larger batches keep 1.5).
+    // NFB_UMMA_MLP_SMS overrides (never above the SM count: the partial
+    // buffers are sized for it).
+    int mlp_sms = c->bcur <= 8 ? (2 * c->sm_count + 2) / 3 : c->sm_count;
+    if (const char* e = getenv("NFB_UMMA_MLP_SMS")) mlp_sms = std::max(1, std::min(c->sm_count, atoi(e)));
+    for (int j = 0; j < 5; ++j)
+      c->uplan[j] = umma_plan(shapes[j][0], 2 * c->bcur, shapes[j][1], (j == 2 || j == 3) ? mlp_sms : c->sm_count);
     c->uplan_rows = c->bcur;
   }
   return NFB_OK;
